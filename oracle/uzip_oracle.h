@@ -1,0 +1,107 @@
+/*
+ * uzip_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded CPU oracle for the Uzip method
+ * (arxiv 2604.17172, "PAPER.md" = /root/reference/PAPER.md).  Only tests/,
+ * __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference)
+ * may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA path under paper_2604_17172_b200/csrc/.
+ *
+ * Every function cites the passage it follows.  Where the paper is silent
+ * the reading taken is the one listed in DESIGN.md "Readings" (R1..R17,
+ * numbered like SURVEY.md 8(c) Q1..Q17).
+ *
+ * Parity status per function:
+ *   uzo_split_elem / uzo_join_elem      pinned (SPEC examples, exhaustive bijection)
+ *   uzo_histogram                       pinned (brute force count)
+ *   uzo_normalize                       pinned (survey g1/g4 tables)
+ *   uzo_encode_block / uzo_decode_block pinned (brute force round trip, information identity)
+ *   uzo_compress / uzo_decompress       pinned (round trip, entropy closed forms, size window)
+ *   uzo_reduce                          pinned (numpy/torch fp32 fold, special-value table)
+ *   exact compressed bytes vs the paper's own implementation: PARITY UNPINNED
+ *   (the paper publishes no format or worked stream).
+ */
+#ifndef UZIP_ORACLE_H
+#define UZIP_ORACLE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype codes (same numbering as include/uzip.h, restated, not shared) */
+enum { UZO_BF16 = 0, UZO_F16 = 1, UZO_F32 = 2 };
+
+/* status codes (same numbering as include/uzip.h, restated, not shared) */
+enum {
+  UZO_OK = 0,
+  UZO_ERR_INVALID_ARG = 1,
+  UZO_ERR_UNSUPPORTED_DTYPE = 2,
+  UZO_ERR_CAPACITY = 3,
+  UZO_ERR_CORRUPT_STREAM = 4,
+  UZO_ERR_SIZE_MISMATCH = 5
+};
+
+/* Format constants of the UZB1 stream. */
+#define UZO_PROB_BITS 12u               /* P: table precision, M = 2^P      */
+#define UZO_M (1u << UZO_PROB_BITS)     /* 4096                             */
+#define UZO_STATE_LBITS 15u             /* L = 2^15, states in [L, 2^31)    */
+#define UZO_L (1u << UZO_STATE_LBITS)
+#define UZO_LANES 32u                   /* W: interleaved states per block  */
+#define UZO_HEADER_BYTES 64u
+#define UZO_RAW_BLOCK 0xFFFFFFFFu       /* directory sentinel: stored raw   */
+
+typedef struct {
+  uint32_t block_symbols;  /* B; multiple of 32; 0 -> default 4096            */
+  uint32_t chunk_blocks;   /* CB; blocks per table chunk; 0 -> 8 MiB / (B*eb) */
+  uint32_t sample_symbols; /* S_s; 0 -> 256 KiB / eb                          */
+  uint32_t global_table;   /* 1 -> one table over every symbol (Step 1) */
+} uzo_params;
+
+size_t uzo_elem_bytes(int dtype);
+
+/* a1 Split: one element -> (symbol, residual).
+ * bits holds the element's raw bits (16 or 32 of them).  For f32 the
+ * residual is 24 bits: lo16 (bits 15..0) | hi8 << 16 where
+ * hi8 = sign<<7 | bits 22..16.  For bf16/f16 the residual is one byte. */
+void uzo_split_elem(int dtype, uint32_t bits, uint8_t *sym, uint32_t *res);
+uint32_t uzo_join_elem(int dtype, uint8_t sym, uint32_t res);
+void uzo_split_array(int dtype, const void *in, size_t n, uint8_t *sym, uint32_t *res);
+void uzo_join_array(int dtype, const uint8_t *sym, const uint32_t *res, size_t n, void *out);
+
+/* a2 Histogram of the first `limit` symbols. */
+void uzo_histogram(const uint8_t *sym, size_t n, size_t limit, uint32_t cnt[256]);
+
+/* a3 Rule N1 normalization to sum M with floor 1 (R5, R6). */
+void uzo_normalize(const uint32_t cnt[256], uint16_t freq[256]);
+
+/* a4 32-lane interleaved rANS encode of one block of B symbols (P:161-165,
+ * P:422-424).  words must hold B entries.  Returns the word count K. */
+uint32_t uzo_encode_block(const uint8_t *sym, uint32_t B, const uint16_t freq[256],
+                          uint32_t states[32], uint16_t *words);
+
+/* a8 decode of one block; returns UZO_OK or UZO_ERR_CORRUPT_STREAM. */
+int uzo_decode_block(const uint32_t states_in[32], const uint16_t *words, uint32_t K,
+                     uint32_t B, const uint16_t freq[256], uint8_t *sym_out);
+
+/* Whole stream (UZB1).  uzo_compress_bound is the capacity that always
+ * suffices. */
+size_t uzo_compress_bound(size_t n, int dtype, const uzo_params *p);
+int uzo_compress(int dtype, const void *in, size_t n, const uzo_params *p,
+                 uint8_t *out, size_t cap, size_t *out_bytes);
+int uzo_decompress(const uint8_t *in, size_t in_bytes, void *out, size_t n, int dtype);
+
+/* a9 fold R (R11): out[i] = rnd(((x0 + x1) + x2) + ...) in fp32, ranks in
+ * order, NaN -> canonical NaN of the dtype. inputs[k] points at rank k's
+ * n elements. */
+void uzo_reduce_sum(int dtype, const void *const *inputs, int nranks, size_t n, void *out);
+
+/* fp32 -> dtype rounding used by the fold (exported for its pin test). */
+uint32_t uzo_round_from_f32(int dtype, float v);
+float uzo_widen_to_f32(int dtype, uint32_t bits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,121 @@
+"""Pins for the 32-lane rANS block coder (a4, a8; R4).
+
+* brute force: lanes are independent given the table, so every lane-0
+  sequence of length R over a 3-symbol alphabet is round-tripped (embedded
+  among random other lanes) under skewed, uniform and floor-only tables;
+* the exact information identity of rANS (each coding step multiplies the
+  state by ~M/f, each emitted word divides it by 2^16):
+      16 K + sum_l log2 x_final[l] - 32*15 - sum_i log2(M / f[s_i]) = eps,
+  |eps| small (rounding of floor(x/f) only) -- a dropped term, a wrong shift
+  or a transposed operand moves eps by hundreds of bits;
+* the byte window that follows from it, SPEC S:143-144 size examples, and
+  corrupt-input behaviour."""
+import itertools
+
+import numpy as np
+import pytest
+
+import synth
+
+
+def _tables():
+    skew = np.ones(256, np.uint16); skew[0x7F] = 4096 - 255 - 300; skew[0x7E] = 201; skew[0x80] = 101
+    unif = np.full(256, 16, np.uint16)
+    floor_only = np.ones(256, np.uint16); floor_only[5] = 4096 - 255      # symbols 0x7E.. have f=1
+    return {"skewed": skew, "uniform": unif, "floor_only": floor_only}
+
+
+@pytest.mark.parametrize("tname", ["skewed", "uniform", "floor_only"])
+def test_bruteforce_lane0_sequences(orc, tname):
+    f = _tables()[tname]
+    assert f.sum() == 4096
+    alphabet = np.array([0x7E, 0x7F, 0x80], np.uint8)
+    R = 9
+    rng = np.random.default_rng(11)
+    others = rng.choice(alphabet, size=(R, 32))
+    for seq in itertools.product(range(3), repeat=R):
+        sym = others.copy()
+        sym[:, 0] = alphabet[list(seq)]
+        sym = sym.reshape(-1)
+        states, words = orc.encode_block(sym, f)
+        st, out = orc.decode_block(states, words, 32 * R, f)
+        assert st == orc.OK and np.array_equal(out, sym)
+
+
+def _info_eps(states, K, f, sym):
+    info = np.sum(np.log2(4096.0 / f[sym].astype(np.float64)))
+    return 16 * K + np.sum(np.log2(states.astype(np.float64))) - 32 * 15 - info
+
+
+@pytest.mark.parametrize("B", [32, 64, 4096, 8192])
+def test_roundtrip_identity_and_window(orc, B):
+    rng = np.random.default_rng(B)
+    for trial in range(25):
+        kind = trial % 5
+        if kind == 0:
+            s, _ = orc.split(0, synth.normal(B, 0.02, trial))
+            f = orc.normalize(orc.histogram(s))
+        elif kind == 1:
+            s, _ = orc.split(0, synth.uniform(B, trial))
+            f = orc.normalize(orc.histogram(s))
+        elif kind == 2:          # random table, symbols drawn from another distribution
+            cnt = rng.integers(0, 1000, 256).astype(np.uint32)
+            f = orc.normalize(cnt)
+            s = rng.integers(0, 256, B).astype(np.uint8)
+        elif kind == 3:          # symbols absent from the table's sample (floor-1)
+            cnt = np.zeros(256, np.uint32); cnt[0x7F] = 5
+            f = orc.normalize(cnt)
+            s = rng.integers(0x70, 0x90, B).astype(np.uint8)
+        else:
+            s = np.full(B, 0x7F, np.uint8)
+            f = orc.normalize(orc.histogram(s))
+        states, words = orc.encode_block(s, f)
+        st, out = orc.decode_block(states, words, B, f)
+        assert st == orc.OK and np.array_equal(out, s)
+        assert np.all(states >= orc.L) and np.all(states < 2 ** 31)
+        eps = _info_eps(states, words.size, f, s)
+        assert abs(eps) <= 6.0, eps
+        sigma_bytes = np.sum(np.log2(4096.0 / f[s].astype(np.float64))) / 8
+        blk = 128 + 2 * words.size
+        assert sigma_bytes + 64 - 1 < blk <= sigma_bytes + 128 + 1
+
+
+def test_survey_g1_g3_sizes(orc):
+    """K = 521, 1184 B; g3 (4096 x 0x7F): K = 0, 128 B, all states equal."""
+    s = synth.lcg_symbols(4096, 12345)
+    f = orc.normalize(orc.histogram(s))
+    states, words = orc.encode_block(s, f)
+    assert words.size == 521 and len(orc.block_bytes(states, words)) == 1184
+    s3 = np.full(4096, 0x7F, np.uint8)
+    f3 = orc.normalize(orc.histogram(s3))
+    states, words = orc.encode_block(s3, f3)
+    assert words.size == 0 and len(orc.block_bytes(states, words)) == 128
+    assert np.all(states == states[0])
+
+
+def test_spec_size_examples(orc):
+    # S:143 4096 copies of one symbol under its skewed table -> <= 64 B of words
+    s = np.full(4096, 0x42, np.uint8)
+    states, words = orc.encode_block(s, orc.normalize(orc.histogram(s)))
+    assert 2 * words.size <= 64
+    # S:144 4096 random symbols under the uniform table -> within 2% of 4096 B
+    rng = np.random.default_rng(5)
+    s = rng.integers(0, 256, 4096).astype(np.uint8)
+    states, words = orc.encode_block(s, np.full(256, 16, np.uint16))
+    assert abs(2 * words.size - 4096) <= 0.02 * 4096   # payload words, flush (states) excluded
+
+
+def test_corrupt_block(orc):
+    s, _ = orc.split(0, synth.normal(4096, 0.02, 9))
+    f = orc.normalize(orc.histogram(s))
+    states, words = orc.encode_block(s, f)
+    st, _ = orc.decode_block(states, words[:-1], 4096, f)       # truncated
+    assert st == orc.ERR_CORRUPT_STREAM
+    st, _ = orc.decode_block(states, np.concatenate([words, [0]]).astype(np.uint16), 4096, f)
+    assert st == orc.ERR_CORRUPT_STREAM
+    bad = states.copy(); bad[3] ^= 0x100
+    st, out = orc.decode_block(bad, words, 4096, f)
+    assert st == orc.ERR_CORRUPT_STREAM or not np.array_equal(out, s)
+    f2 = f.copy(); f2[0x70] += 1; f2[0x7A] -= 1                 # wrong table
+    st, out = orc.decode_block(states, words, 4096, f2)
+    assert st == orc.ERR_CORRUPT_STREAM or not np.array_equal(out, s)
