@@ -1,0 +1,192 @@
+/*
+ * uzip.h -- C ABI of uzip-b200: lossless float compression fused into GPU
+ * communication, after arxiv 2604.17172 ("Uzip"), B200 (sm_100a) only.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * Conventions for every call
+ *  - Buffer pointers are DEVICE pointers (cudaMalloc / torch CUDA memory) on
+ *    the calling thread's current device, 16-byte aligned (128-bit I/O).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Every data call is stream-ordered and asynchronous: it only
+ *    validates arguments on the host and enqueues kernels; no host sync.
+ *  - Synchronous errors are returned (bad pointer/alignment/dtype/size,
+ *    capacity, communicator misuse).  Asynchronous errors found by a kernel
+ *    (corrupt stream, size or dtype mismatch, poll timeout) are written to a
+ *    device status word (`d_status` for uzip_decompress, the communicator's
+ *    error word for collectives, read with uzip_comm_get_async_error).
+ *  - count == 0 is valid and does nothing (returns UZIP_OK).
+ *  - The caller owns all user buffers and must keep them alive until the
+ *    stream work completes.  The library owns communicator staging memory.
+ *
+ * Stream format: UZB1, defined in DESIGN.md section 2 (header with dtype
+ * and sizes before/after compression; residual plane first, P:300-311;
+ * per-chunk tables; block directory; payload; raw tail,
+ * P:458-465).
+ */
+#ifndef UZIP_H
+#define UZIP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define UZIP_API __attribute__((visibility("default")))
+#else
+#define UZIP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Element types the codec splits (fp8 is not in this build). */
+typedef enum { UZIP_BF16 = 0, UZIP_F16 = 1, UZIP_F32 = 2 } uzip_dtype_t;
+
+/* Reduction operators (P:402 names sum, min, max; this build: sum, R11). */
+typedef enum { UZIP_SUM = 0 } uzip_op_t;
+
+typedef enum {
+  UZIP_OK = 0,
+  UZIP_ERR_INVALID_ARG = 1,       /* null/misaligned pointer, bad rank/peer, bad params     */
+  UZIP_ERR_UNSUPPORTED_DTYPE = 2, /* dtype outside uzip_dtype_t                             */
+  UZIP_ERR_CAPACITY = 3,          /* out_capacity < uzip_compress_bound, ws too small       */
+  UZIP_ERR_CORRUPT_STREAM = 4,    /* async: header, table, directory or block check failed  */
+  UZIP_ERR_SIZE_MISMATCH = 5,     /* async: stream n/dtype differ from the call's           */
+  UZIP_ERR_CUDA = 6,              /* a CUDA runtime call failed                              */
+  UZIP_ERR_COMM = 7,              /* communicator setup / bootstrap failure                 */
+  UZIP_ERR_TIMEOUT = 8,           /* async: a peer flag did not arrive in poll_timeout_ms   */
+  UZIP_ERR_NOT_IMPLEMENTED = 9
+} uzip_status_t;
+
+/* Codec parameters; all-zero (or a NULL pointer) selects the defaults.
+ *  block_symbols  B, symbols per independently coded block (Step 2);
+ *                 GPU-supported: 1024, 2048, 4096 (default 4096).
+ *  chunk_blocks   blocks sharing one localized frequency table;
+ *                 default 8 MiB of input; must be a multiple of 8.
+ *  sample_symbols leading symbols of each chunk that build its table
+ *                 ("the first 256 KB"); default 256 KiB of input.
+ *  global_table   1 = one table over every symbol (Step 1). */
+typedef struct uzip_codec_params {
+  uint32_t block_symbols;
+  uint32_t chunk_blocks;
+  uint32_t sample_symbols;
+  uint32_t global_table;
+} uzip_codec_params_t;
+
+/* ---------------------------------------------------------------- codec */
+
+/* Worst-case stream bytes for `count` elements: every block stored raw
+ * (R13).  Returns 0 for an unsupported dtype. */
+UZIP_API size_t uzip_compress_bound(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params);
+
+/* Device workspace bytes needed by uzip_compress / uzip_decompress for
+ * `count` elements.  The workspace must be zero-filled once before first use
+ * (uzip_workspace_init); the kernels leave it reusable.  One workspace must
+ * not be used by two calls in flight at the same time. */
+UZIP_API size_t uzip_workspace_bytes(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params);
+UZIP_API uzip_status_t uzip_workspace_init(void *ws, size_t ws_bytes, void *stream);
+
+/* Compress `count` elements at `in` into one UZB1 stream at `out`
+ * (Steps 1-3 of P:159-170 fused as in P:317-376: split + sampled per-chunk
+ * tables + warp-per-block rANS + look-back compaction, no coalescing pass).
+ * `out_capacity` must be >= uzip_compress_bound.  The stream's byte count is
+ * written to the device word *d_out_bytes when the stream work completes.
+ * Output bytes equal the CPU oracle's for the same input and params. */
+UZIP_API uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, void *out,
+                            size_t out_capacity, uint64_t *d_out_bytes, void *ws, size_t ws_bytes,
+                            const uzip_codec_params_t *params, void *stream);
+
+/* Decompress a UZB1 stream (at most `in_bytes` readable bytes at `in`) into
+ * `count` elements of `dtype` at `out`.  Never reads or writes out of
+ * bounds on corrupt input.  When the stream work
+ * completes, *d_status holds UZIP_OK or the first error found
+ * (UZIP_ERR_CORRUPT_STREAM / UZIP_ERR_SIZE_MISMATCH); on error the contents
+ * of `out` are unspecified. */
+UZIP_API uzip_status_t uzip_decompress(const void *in, size_t in_bytes, void *out, size_t count,
+                              uzip_dtype_t dtype, int32_t *d_status, void *ws, size_t ws_bytes,
+                              void *stream);
+
+/* ---------------------------------------------------------------- communicator */
+
+typedef struct uzip_comm *uzip_comm_t;
+
+/* Host bootstrap all-gather: every rank contributes `bytes_per_rank` bytes
+ * from `send`; `recv` receives nranks*bytes_per_rank bytes in rank order.
+ * Return 0 on success.  (The Python binding supplies torch.distributed.) */
+typedef int (*uzip_allgather_fn)(const void *send, void *recv, size_t bytes_per_rank, void *ctx);
+
+/* Communicator configuration; all-zero or NULL selects defaults.
+ *  min_compress_bytes  compress only messages >= this (R10; default 1 MiB)
+ *  staging_bytes       receive staging per peer, bounds the footprint (default 64 MiB)
+ *  pipe_chunk_bytes    split-send pipeline chunk (P:249-252 large blocks; default 16 MiB)
+ *  max_ctas            CTAs of each fused kernel (0 = all SMs); loopback tests use small values
+ *  poll_timeout_ms     peer-flag wait bound before UZIP_ERR_TIMEOUT (default 10000)
+ *  codec               stream parameters used on the wire */
+typedef struct uzip_config {
+  uint64_t min_compress_bytes;
+  uint64_t staging_bytes;
+  uint64_t pipe_chunk_bytes;
+  uint32_t max_ctas;
+  uint32_t poll_timeout_ms;
+  uzip_codec_params_t codec;
+} uzip_config_t;
+
+/* Multi-process init: one call per rank (one process per GPU), collective
+ * over all ranks through `bootstrap`.  Staging and flag memory is allocated
+ * here and mapped into peers with CUDA IPC ("directly write ...
+ * into the communication buffer"; NVLink P:442). */
+UZIP_API uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_device,
+                             uzip_allgather_fn bootstrap, void *ctx, const uzip_config_t *cfg);
+
+/* Single-process init of `nranks` communicators (like ncclCommInitAll);
+ * devices[r] may repeat (loopback: several ranks on one GPU). */
+UZIP_API uzip_status_t uzip_comm_init_all(uzip_comm_t *comms, int nranks, const int *devices,
+                                 const uzip_config_t *cfg);
+UZIP_API uzip_status_t uzip_comm_destroy(uzip_comm_t comm);
+
+/* Split-send P2P: the residual plane leaves for the peer as soon
+ * as it is split, the entropy-coded exponents follow; the receiver decodes as
+ * blocks land.  A send on rank a matches the next recv on `peer` with the
+ * same count and dtype (FIFO per ordered pair, like NCCL). */
+UZIP_API uzip_status_t uzip_send(const void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t comm,
+                        void *stream);
+UZIP_API uzip_status_t uzip_recv(void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t comm,
+                        void *stream);
+
+/* Compress-on-send / decompress-on-receive collectives, one
+ * direct exchange over NVSwitch (two for allreduce).
+ *  allgather:      recvbuf[r*sendcount + i] = sendbuf_r[i]; one stream per rank sent to all peers
+ *  reduce_scatter: recvbuf_r[i] = R(sendbuf_0[r*recvcount+i], ..., sendbuf_{N-1}[...]) with the
+ *                  fixed-order fp32 fold R (R11); the own shard is never compressed
+ *  allreduce:      two-shot = reduce_scatter + allgather of the reduced shards (count % nranks == 0)
+ * In place: allreduce sendbuf == recvbuf; allgather sendbuf == recvbuf + rank*sendcount;
+ * reduce_scatter recvbuf == sendbuf + rank*recvcount. */
+UZIP_API uzip_status_t uzip_allgather(const void *sendbuf, void *recvbuf, size_t sendcount, uzip_dtype_t dtype,
+                             uzip_comm_t comm, void *stream);
+UZIP_API uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t recvcount,
+                                  uzip_dtype_t dtype, uzip_op_t op, uzip_comm_t comm, void *stream);
+UZIP_API uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype,
+                             uzip_op_t op, uzip_comm_t comm, void *stream);
+
+/* First asynchronous error seen by the communicator's kernels (sync read). */
+UZIP_API uzip_status_t uzip_comm_get_async_error(uzip_comm_t comm, uzip_status_t *err);
+
+/* Byte accounting of the last collective call on this communicator. */
+typedef struct uzip_stats {
+  uint64_t raw_bytes;      /* bytes the call moved logically (uncompressed) */
+  uint64_t wire_bytes;     /* bytes actually stored into peers (after a sync) */
+  uint32_t compressed;     /* 1 if the call took the compressed path */
+  uint32_t reserved;
+} uzip_stats_t;
+UZIP_API uzip_status_t uzip_get_stats(uzip_comm_t comm, uzip_stats_t *out);
+
+UZIP_API const char *uzip_status_string(uzip_status_t s);
+
+/* Library version string, e.g. "uzip-b200 0.1 sm_100a". */
+UZIP_API const char *uzip_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UZIP_H */

@@ -1,0 +1,242 @@
+"""uzip-b200: Python binding of libuzip.so (include/uzip.h), argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module
+converts torch tensors to device pointers and CUDA streams and forwards to the
+C ABI.  There is no CPU fallback: if libuzip.so is missing or no CUDA device is
+visible, the data calls raise.
+
+Method: arxiv 2604.17172 ("Uzip"), §2.1.2 codec, §3.2
+split-send, §3.3-3.4 fused collectives; stream format
+and readings in DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libuzip.so")
+
+BF16, F16, F32 = 0, 1, 2
+SUM = 0
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED_DTYPE", 3: "CAPACITY", 4: "CORRUPT_STREAM",
+          5: "SIZE_MISMATCH", 6: "CUDA", 7: "COMM", 8: "TIMEOUT", 9: "NOT_IMPLEMENTED"}
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED_DTYPE, ERR_CAPACITY, ERR_CORRUPT_STREAM, ERR_SIZE_MISMATCH, \
+    ERR_CUDA, ERR_COMM, ERR_TIMEOUT, ERR_NOT_IMPLEMENTED = range(10)
+
+_TORCH_TO_UZ = {torch.bfloat16: BF16, torch.float16: F16, torch.float32: F32}
+_UZ_TO_TORCH = {v: k for k, v in _TORCH_TO_UZ.items()}
+ELEM_BYTES = {BF16: 2, F16: 2, F32: 4}
+
+EXPORTED = [
+    "uzip_compress_bound", "uzip_workspace_bytes", "uzip_workspace_init", "uzip_compress", "uzip_decompress",
+    "uzip_comm_init", "uzip_comm_init_all", "uzip_comm_destroy", "uzip_send", "uzip_recv", "uzip_allgather",
+    "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
+    "uzip_status_string", "uzip_version",
+]
+
+
+class UzipError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}")
+        self.status = status
+
+
+class CodecParams(ctypes.Structure):
+    _fields_ = [("block_symbols", ctypes.c_uint32), ("chunk_blocks", ctypes.c_uint32),
+                ("sample_symbols", ctypes.c_uint32), ("global_table", ctypes.c_uint32)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("min_compress_bytes", ctypes.c_uint64), ("staging_bytes", ctypes.c_uint64),
+                ("pipe_chunk_bytes", ctypes.c_uint64), ("max_ctas", ctypes.c_uint32),
+                ("poll_timeout_ms", ctypes.c_uint32), ("codec", CodecParams)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("raw_bytes", ctypes.c_uint64), ("wire_bytes", ctypes.c_uint64),
+                ("compressed", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def build(force: bool = False) -> str:
+    return _build.build(force=force)
+
+
+def lib() -> ctypes.CDLL:
+    """Load libuzip.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2604_17172_b200._build` "
+                                  "(uzip has no CPU fallback)")
+            l = ctypes.CDLL(LIB_PATH)
+            vp, sz, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+            pp = ctypes.POINTER(CodecParams)
+            l.uzip_compress_bound.argtypes = [sz, i32, pp]
+            l.uzip_compress_bound.restype = sz
+            l.uzip_workspace_bytes.argtypes = [sz, i32, pp]
+            l.uzip_workspace_bytes.restype = sz
+            l.uzip_workspace_init.argtypes = [vp, sz, vp]
+            l.uzip_compress.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp]
+            l.uzip_decompress.argtypes = [vp, sz, vp, sz, i32, vp, vp, sz, vp]
+            l.uzip_comm_init.argtypes = [ctypes.POINTER(vp), i32, i32, i32, ALLGATHER_FN, vp,
+                                         ctypes.POINTER(Config)]
+            l.uzip_comm_init_all.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(i32), ctypes.POINTER(Config)]
+            l.uzip_comm_destroy.argtypes = [vp]
+            l.uzip_send.argtypes = [vp, sz, i32, i32, vp, vp]
+            l.uzip_recv.argtypes = [vp, sz, i32, i32, vp, vp]
+            l.uzip_allgather.argtypes = [vp, vp, sz, i32, vp, vp]
+            l.uzip_reduce_scatter.argtypes = [vp, vp, sz, i32, i32, vp, vp]
+            l.uzip_allreduce.argtypes = [vp, vp, sz, i32, i32, vp, vp]
+            l.uzip_comm_get_async_error.argtypes = [vp, ctypes.POINTER(i32)]
+            l.uzip_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+            l.uzip_status_string.argtypes = [i32]
+            l.uzip_status_string.restype = ctypes.c_char_p
+            l.uzip_version.restype = ctypes.c_char_p
+            for name in EXPORTED:
+                if name not in ("uzip_compress_bound", "uzip_workspace_bytes", "uzip_status_string", "uzip_version"):
+                    getattr(l, name).restype = i32
+            _lib = l
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise UzipError(st, where)
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _params(block_symbols=0, chunk_blocks=0, sample_symbols=0, global_table=False):
+    return CodecParams(block_symbols, chunk_blocks, sample_symbols, 1 if global_table else 0)
+
+
+def uz_dtype(t: torch.dtype) -> int:
+    if t not in _TORCH_TO_UZ:
+        raise UzipError(ERR_UNSUPPORTED_DTYPE, "dtype")
+    return _TORCH_TO_UZ[t]
+
+
+def torch_dtype(d: int) -> torch.dtype:
+    return _UZ_TO_TORCH[d]
+
+
+# ----------------------------------------------------------------------------- sizing
+def compress_bound(count: int, dtype: int, **params) -> int:
+    p = _params(**params)
+    return lib().uzip_compress_bound(count, dtype, ctypes.byref(p))
+
+
+def workspace_bytes(count: int, dtype: int, **params) -> int:
+    p = _params(**params)
+    return lib().uzip_workspace_bytes(count, dtype, ctypes.byref(p))
+
+
+class Workspace:
+    """Zero-initialized device workspace (uzip_workspace_init), grown on demand."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.buf = None
+
+    def get(self, nbytes: int, stream=None) -> torch.Tensor:
+        nbytes = max(int(nbytes), 64)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes + (nbytes >> 3), dtype=torch.uint8, device=self.device)
+            _check(lib().uzip_workspace_init(ctypes.c_void_p(self.buf.data_ptr()), self.buf.numel(),
+                                             _stream(stream)), "uzip_workspace_init")
+        return self.buf
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, stream=None) -> torch.Tensor:
+    dev = torch.cuda.current_device()
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    ws = _ws_cache.get((dev, s))
+    if ws is None:
+        ws = _ws_cache[(dev, s)] = Workspace(dev)
+    return ws.get(nbytes, stream)
+
+
+# ----------------------------------------------------------------------------- codec
+def uzip_compress(in_ptr, count, dtype, out_ptr, out_capacity, d_out_bytes_ptr, ws_ptr, ws_bytes, params,
+                  stream_ptr) -> int:
+    """Raw C-ABI passthrough (pointers as ints)."""
+    return lib().uzip_compress(in_ptr, count, dtype, out_ptr, out_capacity, d_out_bytes_ptr, ws_ptr, ws_bytes,
+                               ctypes.byref(params) if params is not None else None, stream_ptr)
+
+
+def uzip_decompress(in_ptr, in_bytes, out_ptr, count, dtype, d_status_ptr, ws_ptr, ws_bytes, stream_ptr) -> int:
+    return lib().uzip_decompress(in_ptr, in_bytes, out_ptr, count, dtype, d_status_ptr, ws_ptr, ws_bytes,
+                                 stream_ptr)
+
+
+def compress(x: torch.Tensor, out: torch.Tensor | None = None, out_bytes: torch.Tensor | None = None,
+             stream=None, ws: torch.Tensor | None = None, **params):
+    """Compress a contiguous CUDA tensor; returns (stream bytes tensor, device int64 byte count)."""
+    if not x.is_cuda or not x.is_contiguous():
+        raise UzipError(ERR_INVALID_ARG, "compress: need a contiguous CUDA tensor")
+    dt = uz_dtype(x.dtype)
+    n = x.numel()
+    p = _params(**params)
+    cap = lib().uzip_compress_bound(n, dt, ctypes.byref(p))
+    if cap == 0:
+        raise UzipError(ERR_INVALID_ARG, "compress: unsupported params")
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    if out_bytes is None:
+        out_bytes = torch.zeros(1, dtype=torch.int64, device=x.device)
+    wsb = lib().uzip_workspace_bytes(n, dt, ctypes.byref(p))
+    if ws is None:
+        ws = _workspace(wsb, stream)
+    st = lib().uzip_compress(ctypes.c_void_p(x.data_ptr() if n else 0), n, dt, ctypes.c_void_p(out.data_ptr()),
+                             out.numel(), ctypes.c_void_p(out_bytes.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                             ws.numel(), ctypes.byref(p), _stream(stream))
+    _check(st, "uzip_compress")
+    return out, out_bytes
+
+
+def decompress(stream_buf: torch.Tensor, count: int, dtype, out: torch.Tensor | None = None,
+               status: torch.Tensor | None = None, stream=None, ws: torch.Tensor | None = None,
+               in_bytes: int | None = None):
+    """Decompress a UZB1 stream held in a CUDA uint8 tensor; returns (tensor, device int32 status)."""
+    dt = dtype if isinstance(dtype, int) else uz_dtype(dtype)
+    if out is None:
+        out = torch.empty(count, dtype=torch_dtype(dt), device=stream_buf.device)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=stream_buf.device)
+    if ws is None:
+        ws = _workspace(64, stream)
+    nb = stream_buf.numel() * stream_buf.element_size() if in_bytes is None else in_bytes
+    st = lib().uzip_decompress(ctypes.c_void_p(stream_buf.data_ptr()), nb,
+                               ctypes.c_void_p(out.data_ptr() if count else 0), count, dt,
+                               ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                               _stream(stream))
+    _check(st, "uzip_decompress")
+    return out, status
+
+
+def status_string(st: int) -> str:
+    return lib().uzip_status_string(st).decode()
+
+
+def version() -> str:
+    return lib().uzip_version().decode()

@@ -1,0 +1,100 @@
+// api.cu -- the C ABI of include/uzip.h: host-side argument checks and dispatch.
+// No compute happens here; every data call enqueues kernels on the caller's stream.
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "uzip_internal.h"
+
+using namespace uzip;
+
+namespace uzip {
+
+uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g) {
+  if (dtype < 0 || dtype > 2) return UZIP_ERR_UNSUPPORTED_DTYPE;
+  const uint32_t eb = elem_bytes(dtype);
+  uint32_t B = (p && p->block_symbols) ? p->block_symbols : 4096u;
+  if (!(B == 1024 || B == 2048 || B == 4096)) return UZIP_ERR_INVALID_ARG;
+  const bool global = p && p->global_table;
+  uint32_t CB = (p && p->chunk_blocks) ? p->chunk_blocks : (uint32_t)((8u << 20) / (B * eb));
+  if (CB == 0 || (!global && CB % kTileBlocks != 0)) return UZIP_ERR_INVALID_ARG;
+  uint32_t S = (p && p->sample_symbols) ? p->sample_symbols : (uint32_t)((256u << 10) / eb);
+  g->init(dtype, n, B, CB, S, global);
+  return UZIP_OK;
+}
+
+}  // namespace uzip
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+extern "C" {
+
+const char *uzip_status_string(uzip_status_t s) {
+  switch (s) {
+    case UZIP_OK: return "ok";
+    case UZIP_ERR_INVALID_ARG: return "invalid argument";
+    case UZIP_ERR_UNSUPPORTED_DTYPE: return "unsupported dtype";
+    case UZIP_ERR_CAPACITY: return "output or workspace capacity too small";
+    case UZIP_ERR_CORRUPT_STREAM: return "corrupt stream";
+    case UZIP_ERR_SIZE_MISMATCH: return "stream size or dtype mismatch";
+    case UZIP_ERR_CUDA: return "CUDA error";
+    case UZIP_ERR_COMM: return "communicator error";
+    case UZIP_ERR_TIMEOUT: return "peer flag timeout";
+    case UZIP_ERR_NOT_IMPLEMENTED: return "not implemented";
+  }
+  return "unknown status";
+}
+
+const char *uzip_version(void) { return "uzip-b200 0.1 sm_100a"; }
+
+size_t uzip_compress_bound(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params) {
+  StreamGeom g;
+  if (resolve_geom((int)dtype, count, params, &g) != UZIP_OK) return 0;
+  return (size_t)g.total(g.n_blocks * (uint64_t)g.B);
+}
+
+size_t uzip_workspace_bytes(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params) {
+  StreamGeom g;
+  if (resolve_geom((int)dtype, count, params, &g) != UZIP_OK) return 0;
+  return (size_t)CodecWs::bytes_for(g.n_chunks, g.n_tiles());
+}
+
+uzip_status_t uzip_workspace_init(void *ws, size_t ws_bytes, void *stream) {
+  if (!ws || ws_bytes < 64) return UZIP_ERR_INVALID_ARG;
+  return cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream) == cudaSuccess ? UZIP_OK : UZIP_ERR_CUDA;
+}
+
+uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, void *out, size_t out_capacity,
+                            uint64_t *d_out_bytes, void *ws, size_t ws_bytes, const uzip_codec_params_t *params,
+                            void *stream) {
+  StreamGeom g;
+  uzip_status_t st = resolve_geom((int)dtype, count, params, &g);
+  if (st != UZIP_OK) return st;
+  if (!out || !ws || !aligned16(out) || !aligned16(ws)) return UZIP_ERR_INVALID_ARG;
+  if (count > 0 && (!in || !aligned16(in))) return UZIP_ERR_INVALID_ARG;
+  if (out_capacity < g.total(g.n_blocks * (uint64_t)g.B)) return UZIP_ERR_CAPACITY;
+  if (ws_bytes < CodecWs::bytes_for(g.n_chunks, g.n_tiles())) return UZIP_ERR_CAPACITY;
+  cudaError_t e = launch_compress((int)dtype, in, g, out, d_out_bytes, ws, (cudaStream_t)stream, 0);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "uzip_compress: %s\n", cudaGetErrorString(e));
+    return UZIP_ERR_CUDA;
+  }
+  return UZIP_OK;
+}
+
+uzip_status_t uzip_decompress(const void *in, size_t in_bytes, void *out, size_t count, uzip_dtype_t dtype,
+                              int32_t *d_status, void *ws, size_t ws_bytes, void *stream) {
+  if ((int)dtype < 0 || (int)dtype > 2) return UZIP_ERR_UNSUPPORTED_DTYPE;
+  if (!in || !ws || !d_status || !aligned16(in) || !aligned16(ws)) return UZIP_ERR_INVALID_ARG;
+  if (count > 0 && (!out || !aligned16(out))) return UZIP_ERR_INVALID_ARG;
+  if (ws_bytes < 64) return UZIP_ERR_CAPACITY;
+  cudaError_t e =
+      launch_decompress((int)dtype, in, in_bytes, out, count, ws, d_status, (cudaStream_t)stream, 0);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "uzip_decompress: %s\n", cudaGetErrorString(e));
+    return UZIP_ERR_CUDA;
+  }
+  return UZIP_OK;
+}
+
+}  // extern "C"

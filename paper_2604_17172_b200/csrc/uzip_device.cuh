@@ -1,0 +1,229 @@
+// uzip_device.cuh -- device-side building blocks of the Uzip codec for sm_100a.
+//
+// This is the CUDA path's own restatement of the method (it shares nothing with
+// oracle/): the float split of Step 1, the localized tables
+// of P:357-370, warp-per-block rANS and the decode
+// (P:391).  Stream layout: DESIGN.md section 2.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace uzip {
+
+// ---------------------------------------------------------------- format constants
+constexpr uint32_t kProbBits = 12;             // P (table precision)
+constexpr uint32_t kM = 1u << kProbBits;        // 4096
+constexpr uint32_t kLBits = 15;                 // states live in [2^15, 2^31)
+constexpr uint32_t kL = 1u << kLBits;
+constexpr uint32_t kLanes = 32;                 // interleaved states per block (one warp)
+constexpr uint32_t kHeaderBytes = 64;
+constexpr uint32_t kRawBlock = 0xFFFFFFFFu;
+constexpr uint32_t kVersion = 1;
+constexpr int kWarps = 8;                       // warps per CTA in the codec kernels
+constexpr uint32_t kTileBlocks = kWarps;        // blocks per look-back tile
+constexpr uint32_t kMaxB = 4096;                // largest block the GPU kernels stage in smem
+constexpr uint32_t kHistSymsPerCta = 16384;     // sampled symbols per k_table CTA
+
+enum Dtype : int { kBF16 = 0, kF16 = 1, kF32 = 2 };
+
+__host__ __device__ constexpr uint32_t elem_bytes(int dt) { return dt == kF32 ? 4u : 2u; }
+__host__ __device__ constexpr uint64_t round16(uint64_t v) { return (v + 15u) & ~uint64_t(15); }
+
+// Section offsets of a UZB1 stream, computed the same way
+// on host and device from the header fields.
+struct StreamGeom {
+  uint64_t n, n_blocks, n_coded, n_chunks;
+  uint32_t B, CB, S, global, dtype, eb;
+  uint64_t off_res0, off_res1, off_tab, off_coff, off_dir, off_pay;
+
+  __host__ __device__ void init(int dt, uint64_t n_, uint32_t B_, uint32_t CB_, uint32_t S_, bool global_) {
+    dtype = (uint32_t)dt;
+    eb = elem_bytes(dt);
+    n = n_;
+    B = B_;
+    n_blocks = n / B;
+    n_coded = n_blocks * B;
+    global = global_ ? 1u : 0u;
+    if (global_) {
+      CB = n_blocks ? (uint32_t)n_blocks : 1u;
+      S = 0;
+    } else {
+      CB = CB_;
+      S = S_;
+    }
+    n_chunks = (n_blocks + CB - 1) / CB;
+    off_res0 = kHeaderBytes;
+    if (dt == kF32) {
+      off_res1 = off_res0 + 2 * n_coded;
+      off_tab = round16(off_res1 + n_coded);
+    } else {
+      off_res1 = off_res0;
+      off_tab = round16(off_res0 + n_coded);
+    }
+    off_coff = off_tab + 512 * n_chunks;
+    off_dir = round16(off_coff + 8 * n_chunks);
+    off_pay = round16(off_dir + 4 * n_blocks);
+  }
+  __host__ __device__ uint64_t off_tail(uint64_t payload) const { return round16(off_pay + payload); }
+  __host__ __device__ uint64_t total(uint64_t payload) const { return off_tail(payload) + (n - n_coded) * eb; }
+  __host__ __device__ uint64_t n_tiles() const { return (n_blocks + kTileBlocks - 1) / kTileBlocks; }
+  __host__ __device__ uint32_t chunk_blocks_of(uint64_t c) const {
+    uint64_t left = n_blocks - c * CB;
+    return (uint32_t)(left < CB ? left : CB);
+  }
+  __host__ __device__ uint32_t sample_len(uint64_t c) const {
+    uint64_t syms = (uint64_t)chunk_blocks_of(c) * B;
+    return (uint32_t)((S == 0 || S > syms) ? syms : S);
+  }
+};
+
+// Workspace carve-up (host and device agree; control words first).
+struct CodecWs {
+  uint32_t *ticket;       // k_encode tile ticket (zeroed by k_table)
+  uint32_t *err;          // k_decode first error (self-resetting)
+  uint32_t *dec_arrive;   // k_decode CTA arrivals (self-resetting)
+  uint32_t *arrive;       // k_table per-chunk arrivals (self-resetting)
+  uint32_t *counts;       // k_table per-chunk histogram (self-resetting)
+  uint4 *enc;             // per-chunk encode tables {rcp, f<<19|shift, bias, M-f}
+  unsigned long long *tile_status;  // look-back words (zeroed by k_table)
+
+  __host__ __device__ static uint64_t bytes_for(uint64_t n_chunks, uint64_t n_tiles) {
+    uint64_t b = 64;                       // control words
+    b += round16(4 * n_chunks);            // arrive
+    b += 1024 * n_chunks;                  // counts
+    b += 4096 * n_chunks;                  // enc
+    b += 8 * n_tiles;                      // tile status
+    return round16(b);
+  }
+  __host__ __device__ static CodecWs carve(void *base, uint64_t n_chunks) {
+    CodecWs w;
+    uint8_t *p = (uint8_t *)base;
+    w.ticket = (uint32_t *)(p + 0);
+    w.err = (uint32_t *)(p + 4);
+    w.dec_arrive = (uint32_t *)(p + 8);
+    p += 64;
+    w.arrive = (uint32_t *)p;
+    p += round16(4 * n_chunks);
+    w.counts = (uint32_t *)p;
+    p += 1024 * n_chunks;
+    w.enc = (uint4 *)p;
+    p += 4096 * n_chunks;
+    w.tile_status = (unsigned long long *)p;
+    return w;
+  }
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_nc_v2(const void *p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_nc_u32(const void *p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+  unsigned long long r;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t *p) {
+  uint32_t r;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// ---------------------------------------------------------------- a1 split / join
+// Split of one 16-byte vector into symbols and residual (DESIGN.md
+// section 2).  Byte-permute forms: 1.5 ALU ops per element.
+// bf16 (s:15 e:14..7 m:6..0): symbol = e, residual = s<<7 | m.
+__device__ __forceinline__ void split4_bf16(uint32_t w0, uint32_t w1, uint32_t &sym4, uint32_t &res4) {
+  sym4 = __byte_perm(w0 >> 7, w1 >> 7, 0x6420);
+  uint32_t lo = __byte_perm(w0, w1, 0x6420);
+  uint32_t hi = __byte_perm(w0, w1, 0x7531);
+  res4 = (lo & 0x7F7F7F7Fu) | (hi & 0x80808080u);
+}
+// f16: symbol = high byte, residual = low byte (R3).
+__device__ __forceinline__ void split4_f16(uint32_t w0, uint32_t w1, uint32_t &sym4, uint32_t &res4) {
+  sym4 = __byte_perm(w0, w1, 0x7531);
+  res4 = __byte_perm(w0, w1, 0x6420);
+}
+// f32 (s:31 e:30..23 m:22..0): symbol = e, lo16 = m[15:0], hi8 = s<<7 | m[22:16].
+__device__ __forceinline__ void split4_f32(uint4 w, uint32_t &sym4, uint2 &lo, uint32_t &hi4) {
+  uint32_t a = __byte_perm(w.x >> 23, w.y >> 23, 0x0040);
+  uint32_t b = __byte_perm(w.z >> 23, w.w >> 23, 0x0040);
+  sym4 = __byte_perm(a, b, 0x5410);
+  lo.x = __byte_perm(w.x, w.y, 0x5410);
+  lo.y = __byte_perm(w.z, w.w, 0x5410);
+  uint32_t x01 = __byte_perm(w.x, w.y, 0x7362);
+  uint32_t x23 = __byte_perm(w.z, w.w, 0x7362);
+  uint32_t b2 = __byte_perm(x01, x23, 0x5410);
+  uint32_t b3 = __byte_perm(x01, x23, 0x7632);
+  hi4 = (b2 & 0x7F7F7F7Fu) | (b3 & 0x80808080u);
+}
+
+__device__ __forceinline__ void join4_bf16(uint32_t sym4, uint32_t res4, uint32_t &w0, uint32_t &w1) {
+  uint32_t hb = (res4 & 0x80808080u) | ((sym4 >> 1) & 0x7F7F7F7Fu);
+  uint32_t lb = ((sym4 << 7) & 0x80808080u) | (res4 & 0x7F7F7F7Fu);
+  w0 = __byte_perm(lb, hb, 0x5140);
+  w1 = __byte_perm(lb, hb, 0x7362);
+}
+__device__ __forceinline__ void join4_f16(uint32_t sym4, uint32_t res4, uint32_t &w0, uint32_t &w1) {
+  w0 = __byte_perm(res4, sym4, 0x5140);
+  w1 = __byte_perm(res4, sym4, 0x7362);
+}
+__device__ __forceinline__ uint4 join4_f32(uint32_t sym4, uint2 lo, uint32_t hi4) {
+  uint32_t b2 = ((sym4 << 7) & 0x80808080u) | (hi4 & 0x7F7F7F7Fu);
+  uint32_t b3 = (hi4 & 0x80808080u) | ((sym4 >> 1) & 0x7F7F7F7Fu);
+  uint32_t h01 = __byte_perm(b2, b3, 0x5140);
+  uint32_t h23 = __byte_perm(b2, b3, 0x7362);
+  uint4 r;
+  r.x = __byte_perm(lo.x, h01, 0x5410);
+  r.y = __byte_perm(lo.x, h01, 0x7632);
+  r.z = __byte_perm(lo.y, h23, 0x5410);
+  r.w = __byte_perm(lo.y, h23, 0x7632);
+  return r;
+}
+
+// ---------------------------------------------------------------- a3 encode table entry
+// rANS encode needs floor(x/f) for x < f*2^19 < 2^31: a 32-bit reciprocal
+// with shift s-1 (s = ceil(log2 f)) is exact below 2^31; f = 1 uses
+// rcp = 2^32-1 (q = x-1) with the bias raised by M-1.  Entry:
+//   x = rcp, y = f<<19 | shift (renorm threshold + funnel-shift amount),
+//   z = bias, w = M - f.
+__host__ __device__ inline uint4 make_enc_entry(uint32_t f, uint32_t cdf) {
+  uint4 e;
+  if (f < 2) {
+    e.x = 0xFFFFFFFFu;
+    e.y = (f << 19) | 0u;
+    e.z = cdf + kM - 1;
+  } else {
+    uint32_t s = 0;
+    while (f > (1u << s)) ++s;
+    e.x = (uint32_t)(((1ull << (s + 31)) + f - 1) / f);
+    e.y = (f << 19) | (s - 1);
+    e.z = cdf;
+  }
+  e.w = kM - f;
+  return e;
+}
+
+}  // namespace uzip

@@ -1,0 +1,19 @@
+// uzip_internal.h -- declarations shared by the CUDA translation units of libuzip.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/uzip.h"
+#include "uzip_device.cuh"
+
+namespace uzip {
+
+cudaError_t launch_compress(int dtype, const void *in, const StreamGeom &g, void *out, uint64_t *d_out_bytes,
+                            void *ws, cudaStream_t st, int max_ctas);
+cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void *out, uint64_t n, void *ws,
+                              int32_t *d_status, cudaStream_t st, int max_ctas);
+
+// Resolve codec params (defaults of DESIGN.md section 2) into a geometry; returns
+// UZIP_OK or UZIP_ERR_INVALID_ARG for unsupported values.
+uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g);
+
+}  // namespace uzip

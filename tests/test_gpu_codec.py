@@ -1,0 +1,208 @@
+"""GPU parity of the codec kernels against the CPU oracle, through the C ABI.
+
+Bit-exact: GPU stream bytes == oracle stream bytes, GPU decode == input bytes,
+across dtypes x sizes (empty, ragged, several tiles and chunks) x value
+distributions x stream parameters; BASELINE C1 (4 MiB bf16 W) in full; the
+1 GiB C2 shard (the bench launch configuration) by exact round trip plus
+sampled tables and blocks recomputed one by one by the oracle; corrupt-stream
+behaviour."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+BF16, F16, F32 = 0, 1, 2
+TD = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32}
+VIEW = {BF16: torch.int16, F16: torch.int16, F32: torch.int32}
+
+
+@pytest.fixture(scope="module")
+def uz():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_17172_b200 as uz
+    uz.build()
+    return uz
+
+
+def to_dev(bits: np.ndarray, dtype: int) -> torch.Tensor:
+    t = torch.from_numpy(bits.view(np.int32 if dtype == F32 else np.int16).copy())
+    return t.view(TD[dtype]).cuda()
+
+
+def to_bits(t: torch.Tensor, dtype: int) -> np.ndarray:
+    return t.view(VIEW[dtype]).cpu().numpy().view(np.uint32 if dtype == F32 else np.uint16)
+
+
+def gpu_compress(uz, bits, dtype, **params) -> bytes:
+    x = to_dev(bits, dtype) if bits.size else torch.empty(0, dtype=TD[dtype], device="cuda")
+    out, nbytes = uz.compress(x, **params)
+    torch.cuda.synchronize()
+    return out[: int(nbytes.item())].cpu().numpy().tobytes()
+
+
+def gpu_decompress(uz, stream: bytes, n, dtype, in_bytes=None):
+    buf = torch.from_numpy(np.frombuffer(stream, np.uint8).copy()).cuda() if stream else \
+        torch.zeros(16, dtype=torch.uint8, device="cuda")
+    out, st = uz.decompress(buf, n, dtype, in_bytes=in_bytes)
+    torch.cuda.synchronize()
+    return int(st.item()), (to_bits(out, dtype) if n else np.zeros(0))
+
+
+GENS = {
+    "W": lambda n, s, d: synth.normal(n, 0.02, s, d),
+    "U": lambda n, s, d: synth.uniform(n, s, d),
+    "special": lambda n, s, d: synth.special_mix(n, s, d),
+    "random": lambda n, s, d: synth.random_bits(n, s, d),
+    "zeros": lambda n, s, d: synth.constant(n, 0, d),
+}
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("n", [0, 1, 4095, 4096, 4097, 3 * 4096 + 17, 40 * 4096 + 5])
+@pytest.mark.parametrize("dist", list(GENS))
+def test_stream_bytes_equal_oracle(uz, orc, dtype, n, dist):
+    bits = GENS[dist](n, 1000 + n, dtype)
+    ref = orc.compress(dtype, bits)
+    got = gpu_compress(uz, bits, dtype)
+    assert len(got) == len(ref)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, n, dtype)
+    assert st == 0 and np.array_equal(back, bits)
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("params", [dict(block_symbols=1024), dict(block_symbols=2048),
+                                    dict(global_table=True), dict(chunk_blocks=8, sample_symbols=1000),
+                                    dict(chunk_blocks=16, sample_symbols=70001, block_symbols=1024),
+                                    dict(global_table=True, block_symbols=1024)])
+def test_stream_params_equal_oracle(uz, orc, dtype, params):
+    n = 37 * 4096 + 11
+    bits = synth.normal(n, 0.02, 7, dtype)
+    bits[4096 * 20:4096 * 21] = synth.random_bits(4096, 8, dtype)
+    ref = orc.compress(dtype, bits, **params)
+    got = gpu_compress(uz, bits, dtype, **params)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, n, dtype)
+    assert st == 0 and np.array_equal(back, bits)
+
+
+def test_c1_full_4mib_bf16(uz, orc):
+    """BASELINE configs[0]: one 4 MiB bf16 ~N(0,0.02) tensor, full oracle parity."""
+    n = 2 * 1024 * 1024
+    bits = synth.weights(n, 1000)
+    ref = orc.compress(BF16, bits)
+    got = gpu_compress(uz, bits, BF16)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, n, BF16)
+    assert st == 0 and np.array_equal(back, bits)
+    assert abs(len(got) / (2 * n) - 0.678) < 0.005
+
+
+@pytest.mark.parametrize("dtype", [BF16, F32])
+def test_multichunk_48mib(uz, orc, dtype):
+    n = (48 << 20) // (2 if dtype == BF16 else 4) + 123
+    bits = synth.normal(n, 0.02, 3, dtype)
+    assert gpu_compress(uz, bits, dtype) == orc.compress(dtype, bits)
+
+
+def test_golden_streams_decode(uz):
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    for case in json.load(open(os.path.join(gold, "manifest.json")))["cases"]:
+        bits = np.load(os.path.join(gold, case["name"] + ".npy"))
+        stream = open(os.path.join(gold, case["name"] + ".uzb"), "rb").read()
+        st, back = gpu_decompress(uz, stream, case["n"], case["dtype"])
+        assert st == 0 and np.array_equal(back, bits), case["name"]
+        assert gpu_compress(uz, bits, case["dtype"], **case["params"]) == stream, case["name"]
+
+
+def test_workspace_reuse_and_repeat(uz, orc):
+    bits = synth.normal(9 * 4096 + 3, 0.02, 5)
+    ref = orc.compress(BF16, bits)
+    for _ in range(3):
+        assert gpu_compress(uz, bits, BF16) == ref
+    small = synth.normal(4096 * 2, 0.02, 6)
+    assert gpu_compress(uz, small, BF16) == orc.compress(BF16, small)
+    assert gpu_compress(uz, bits, BF16) == ref
+
+
+def test_corrupt_and_mismatch(uz, orc):
+    n = 12 * 4096 + 7
+    bits = synth.normal(n, 0.02, 9)
+    s = gpu_compress(uz, bits, BF16)
+    assert gpu_decompress(uz, s, n + 1, BF16)[0] == uz.ERR_SIZE_MISMATCH
+    assert gpu_decompress(uz, s, n, F16)[0] == uz.ERR_SIZE_MISMATCH
+    assert gpu_decompress(uz, s, n, BF16, in_bytes=len(s) - 16)[0] == uz.ERR_CORRUPT_STREAM
+    assert gpu_decompress(uz, s[:32], n, BF16)[0] == uz.ERR_CORRUPT_STREAM
+    sec = orc.sections(s)
+    rng = np.random.default_rng(1)
+    for trial in range(200):
+        bad = bytearray(s)
+        region = trial % 4
+        if region == 0:
+            pos = int(rng.integers(0, 64))
+        elif region == 1:
+            pos = int(rng.integers(sec["off_tab"], sec["off_pay"]))
+        else:
+            pos = int(rng.integers(sec["off_pay"], sec["off_tail"]))
+        bad[pos] ^= 1 << int(rng.integers(0, 8))
+        st, out = gpu_decompress(uz, bytes(bad), n, BF16)
+        ost, oout = orc.decompress(bytes(bad), n, BF16)
+        # the GPU decoder rejects exactly what the oracle rejects
+        assert (st == 0) == (ost == 0), (pos, st, ost)
+        if st == 0:
+            assert np.array_equal(out, oout)
+    # the status word is reset: a good stream decodes OK again
+    st, back = gpu_decompress(uz, s, n, BF16)
+    assert st == 0 and np.array_equal(back, bits)
+
+
+def test_c2_full_size_1gib_sampled(uz, orc):
+    """BASELINE configs[1] shard (1 GiB bf16 W) in the bench's launch config:
+    exact on-device round trip; tables and sampled blocks recomputed by the oracle."""
+    n = 512 * 1024 * 1024
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1001)
+    x = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    out, nbytes = uz.compress(x)
+    y, st = uz.decompress(out, n, BF16)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert torch.equal(x.view(torch.int16), y.view(torch.int16))
+    total = int(nbytes.item())
+    assert abs(total / (2 * n) - 0.678) < 0.005
+    stream = out[:total].cpu().numpy()
+    sec = orc.sections(stream[:64].tobytes() + b"")
+    nb, nc, B, CB = sec["n_blocks"], sec["n_chunks"], sec["B"], sec["CB"]
+    assert (nb, nc) == (131072, 128)
+    dirv = stream[sec["off_dir"]:sec["off_dir"] + 4 * nb].view("<u4")
+    coff = stream[sec["off_coff"]:sec["off_coff"] + 8 * nc].view("<u8")
+    sizes = np.where(dirv == orc.RAW_BLOCK, B, (128 + 2 * dirv.astype(np.int64) + 15) // 16 * 16)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    assert np.array_equal(coff, offs[np.arange(nc) * CB])
+    assert offs[-1] == sec["payload_bytes"]
+    xb = x.view(torch.int16)
+    for c in (0, 1, 63, 127):
+        sample = xb[c * CB * B: c * CB * B + 131072].cpu().numpy().view(np.uint16)
+        sym, _ = orc.split(BF16, sample)
+        f_ref = orc.normalize(orc.histogram(sym))
+        f_gpu = stream[sec["off_tab"] + 512 * c: sec["off_tab"] + 512 * (c + 1)].view("<u2")
+        assert np.array_equal(f_ref, f_gpu), c
+    rng = np.random.default_rng(0)
+    for b in [0, 1, CB - 1, CB, nb - 1] + list(rng.integers(0, nb, 24)):
+        b = int(b)
+        c = b // CB
+        blk = xb[b * B:(b + 1) * B].cpu().numpy().view(np.uint16)
+        sym, res = orc.split(BF16, blk)
+        f = stream[sec["off_tab"] + 512 * c: sec["off_tab"] + 512 * (c + 1)].view("<u2")
+        states, words = orc.encode_block(sym, f)
+        ref = orc.block_bytes(states, words)
+        assert dirv[b] == words.size
+        got = stream[sec["off_pay"] + offs[b]: sec["off_pay"] + offs[b] + sizes[b]].tobytes()
+        assert got == ref, b
+        assert np.array_equal(stream[sec["off_res0"] + b * B: sec["off_res0"] + (b + 1) * B], res.astype(np.uint8))
