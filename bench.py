@@ -1,0 +1,327 @@
+"""bench.py -- uzip-b200 benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl uzip|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+Metric (BASELINE.json): effective uncompressed GB/s = raw bytes / time (GB = 1e9 B,
+SURVEY 8(d)), plus the compression ratio.
+
+N = 1 workload "c2_shard_codec_roundtrip": one step = the single-GPU part of
+BASELINE configs[1] -- the 1 GiB bf16 N(0, 0.02) weight shard compressed
+(uzip_compress: k_table + k_encode, rows a1-a5) and decompressed
+(uzip_decompress: k_decode, rows a7-a8) through the C ABI.  Inputs (1 GiB) are
+larger than L2 (126 MB), so no flush is needed between steps.
+
+N > 1 workload "c2_p2p_pairs" (one process per GPU): ranks (2i, 2i+1) run the
+split-send P2P of a 1 GiB bf16 shard 2i -> 2i+1 (uzip_send / uzip_recv, rows
+a1-a8, a12); value = raw bytes all pairs moved / max-over-ranks time (weak).
+
+--impl reference: the CPU oracle (oracle/, the only reference this tier has)
+on a bounded sample of the same workload, timed on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GB = 1e9
+BF16 = 0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="uzip", choices=["uzip", "reference"])
+    ap.add_argument("--bytes", type=int, default=1 << 30, help="raw bytes per message (default 1 GiB)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+def cpu_baseline(sample_bytes: int = 16 << 20, seed: int = 1001):
+    """The oracle as it stands (single thread) on a bounded sample of the W input."""
+    import numpy as np
+    import oracle
+    import synth
+    oracle.build()
+    n = sample_bytes // 2
+    bits = synth.weights(n, seed)
+    t0 = time.perf_counter()
+    s = oracle.compress(BF16, bits)
+    st, back = oracle.decompress(s, n, BF16)
+    dt = time.perf_counter() - t0
+    assert st == 0 and np.array_equal(back, bits)
+    return {"value": round(sample_bytes / dt / GB, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{sample_bytes >> 20} MiB bf16 N(0,0.02) compress+decompress, single-threaded C oracle",
+            "seconds": round(dt, 3), "ratio": round(len(s) / sample_bytes, 5)}
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle on a bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synth
+    oracle.build()
+    sample = 8 << 20
+    n = sample // 2
+    bits = synth.weights(n, 1001)
+    for _ in range(args.warmup):
+        oracle.decompress(oracle.compress(BF16, bits), n, BF16)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        s = oracle.compress(BF16, bits)
+        st, back = oracle.decompress(s, n, BF16)
+        times.append(time.perf_counter() - t0)
+        assert st == 0
+    ms = 1e3 * sum(times) / len(times)
+    val = sample / (ms / 1e3) / GB
+    line = {"impl": "reference", "metric": "effective uncompressed GB/s", "value": round(val, 5), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "config": config_for(args, sample_note=f"{sample >> 20} MiB sample per step"),
+            "cpu_baseline": {"value": round(val, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{sample >> 20} MiB bf16 W compress+decompress per step"},
+            "e2e": {"value": round(val, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "compression_ratio": round(len(s) / sample, 5)}
+    print(json.dumps(line), flush=True)
+
+
+def config_for(args, sample_note=None):
+    if args.gpus == 1:
+        c = {"workload": "c2_shard_codec_roundtrip", "message_bytes": args.bytes, "dtype": "bf16",
+             "data": "W = bf16(N(0,0.02))", "l2": "inputs 1 GiB > L2 126 MB, no flush",
+             "parallelism": "single GPU"}
+    else:
+        c = {"workload": "c2_p2p_pairs", "message_bytes": args.bytes, "dtype": "bf16",
+             "data": "W = bf16(N(0,0.02))", "l2": "inputs 1 GiB > L2 126 MB, no flush",
+             "parallelism": f"{args.gpus // 2} split-send pairs"}
+    if sample_note:
+        c["sample"] = sample_note
+    return c
+
+
+# ----------------------------------------------------------------------------- uzip arm, N = 1
+def run_codec(args):
+    import torch
+    import paper_2604_17172_b200 as uz
+    uz.build()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n = args.bytes // 2
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1001)
+    x = (torch.randn(n, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    cap = uz.compress_bound(n, uz.BF16)
+    out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    nbytes = torch.zeros(1, dtype=torch.int64, device=dev)
+    y = torch.empty_like(x)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    ws = uz.Workspace(0).get(uz.workspace_bytes(n, uz.BF16), stream)
+    torch.cuda.synchronize()
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        uz.compress(x, out=out, out_bytes=nbytes, stream=stream, ws=ws)
+        if ev is not None:
+            ev[1].record(stream)
+        uz.decompress(out, n, uz.BF16, out=y, status=st, stream=stream, ws=ws)
+        if ev is not None:
+            ev[2].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0 and torch.equal(x.view(torch.int16), y.view(torch.int16)), "round trip failed"
+    total = int(nbytes.item())
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(stop) / args.steps
+    enc_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    dec_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    assert int(st.item()) == 0
+    raw = n * 2
+    r = total / raw
+    hbm, src = peaks()
+    enc_bytes = raw + total           # read input, write stream (algorithmic)
+    dec_bytes = total + raw           # read stream, write output
+    enc_gbs = enc_bytes / (enc_ms / 1e3) / GB
+    dec_gbs = dec_bytes / (dec_ms / 1e3) / GB
+    dom = ("k_table+k_encode (uzip_compress)", enc_gbs, enc_bytes) if enc_ms >= dec_ms else \
+        ("k_decode (uzip_decompress)", dec_gbs, dec_bytes)
+
+    # memcpy reference on the same box (context): torch copy_ of the same bytes
+    z = torch.empty_like(x)
+    for _ in range(3):
+        z.copy_(x)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        z.copy_(x)
+    e1.record()
+    torch.cuda.synchronize()
+    copy_gbs = 2 * raw / (e0.elapsed_time(e1) / 5 / 1e3) / GB
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_codec_e2e(uz, x, args, stream)
+
+    line = {
+        "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": config_for(args),
+        "compression_ratio": round(r, 5),
+        "encode": {"ms": round(enc_ms, 4), "uncompressed_GBps": round(raw / (enc_ms / 1e3) / GB, 2),
+                   "hbm_GBps": round(enc_gbs, 1)},
+        "decode": {"ms": round(dec_ms, 4), "uncompressed_GBps": round(raw / (dec_ms / 1e3) / GB, 2),
+                   "hbm_GBps": round(dec_gbs, 1)},
+        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": round(dom[1], 1), "peak": hbm,
+                     "peak_source": src, "unit": "GB/s", "frac": round(dom[1] / hbm, 4), "traffic": None,
+                     "algorithmic_bytes_per_launch": dom[2]},
+        "torch_copy_GBps": round(copy_gbs, 1),
+        "clocks": clk.summary(),
+        "gpu_launches": 3 * args.steps,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def run_codec_e2e(uz, x, args, stream):
+    """Same metric through the public API with host buffers: pinned H2D of the input, compress,
+    decompress, D2H of the status word and stream size, all inside the timed region."""
+    import torch
+    n = x.numel()
+    host = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+    host.copy_(x.cpu())
+    xd = torch.empty_like(x)
+    cap = uz.compress_bound(n, uz.BF16)
+    out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    nbytes = torch.zeros(1, dtype=torch.int64, device=x.device)
+    y = torch.empty_like(x)
+    st = torch.zeros(1, dtype=torch.int32, device=x.device)
+    res_h = torch.empty(2, dtype=torch.int64, pin_memory=True)
+    ws = uz.Workspace(0).get(uz.workspace_bytes(n, uz.BF16), stream)
+    res_d = torch.empty(2, dtype=torch.int64, device=x.device)
+
+    def step():
+        with torch.cuda.stream(stream):
+            xd.copy_(host, non_blocking=True)
+            uz.compress(xd, out=out, out_bytes=nbytes, stream=stream, ws=ws)
+            uz.decompress(out, n, uz.BF16, out=y, status=st, stream=stream, ws=ws)
+            res_d[0:1].copy_(nbytes)
+            res_d[1:2].copy_(st)
+            res_h.copy_(res_d, non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(2):
+        step()
+    steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    assert int(res_h[1]) == 0
+    return {"value": round(2 * n / dt / GB, 3), "unit": "GB/s", "h2d_bytes_per_step": 2 * n,
+            "d2h_bytes_per_step": 16, "ms_per_step": round(dt * 1e3, 3)}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    if args.gpus == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        run_codec(args)
+    else:
+        import bench_dist
+        bench_dist.run(args)
+
+
+if __name__ == "__main__":
+    main()

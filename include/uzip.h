@@ -118,8 +118,9 @@ typedef int (*uzip_allgather_fn)(const void *send, void *recv, size_t bytes_per_
 
 /* Communicator configuration; all-zero or NULL selects defaults.
  *  min_compress_bytes  compress only messages >= this (R10; default 1 MiB)
- *  staging_bytes       receive staging per peer, bounds the footprint (default 64 MiB)
- *  pipe_chunk_bytes    split-send pipeline chunk (P:249-252 large blocks; default 16 MiB)
+ *  staging_bytes       receive staging per peer = 2 slots, bounds the footprint (default 512 MiB)
+ *  pipe_chunk_bytes    largest round (one UZB1 stream) in input bytes (P:249-252 large blocks;
+ *                      default: as large as a slot allows)
  *  max_ctas            CTAs of each fused kernel (0 = all SMs); loopback tests use small values
  *  poll_timeout_ms     peer-flag wait bound before UZIP_ERR_TIMEOUT (default 10000)
  *  codec               stream parameters used on the wire */
@@ -172,14 +173,23 @@ UZIP_API uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t
 /* First asynchronous error seen by the communicator's kernels (sync read). */
 UZIP_API uzip_status_t uzip_comm_get_async_error(uzip_comm_t comm, uzip_status_t *err);
 
-/* Byte accounting of the last collective call on this communicator. */
+/* Byte accounting of the last call on this communicator (sync read).
+ * raw_bytes: bytes this rank would have stored into peers uncompressed;
+ * wire_bytes: bytes it actually stored (UZB1 streams: header, tables and
+ * directory included, R17).  wire/raw is the call's compression ratio. */
 typedef struct uzip_stats {
-  uint64_t raw_bytes;      /* bytes the call moved logically (uncompressed) */
-  uint64_t wire_bytes;     /* bytes actually stored into peers (after a sync) */
+  uint64_t raw_bytes;
+  uint64_t wire_bytes;
   uint32_t compressed;     /* 1 if the call took the compressed path */
   uint32_t reserved;
 } uzip_stats_t;
 UZIP_API uzip_status_t uzip_get_stats(uzip_comm_t comm, uzip_stats_t *out);
+
+/* Debug/test: copy the first `bytes` of the staging slot (0 or 1) where
+ * rank `src`'s rounds land on this rank into host memory (sync).  Round q of
+ * the ordered pair (src, this rank) lands in slot q % 2 as one UZB1 stream
+ * (the oracle's wire stream). */
+UZIP_API uzip_status_t uzip_comm_read_staging(uzip_comm_t comm, int src, int slot, void *host, size_t bytes);
 
 UZIP_API const char *uzip_status_string(uzip_status_t s);
 

@@ -37,7 +37,7 @@ EXPORTED = [
     "uzip_compress_bound", "uzip_workspace_bytes", "uzip_workspace_init", "uzip_compress", "uzip_decompress",
     "uzip_comm_init", "uzip_comm_init_all", "uzip_comm_destroy", "uzip_send", "uzip_recv", "uzip_allgather",
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
-    "uzip_status_string", "uzip_version",
+    "uzip_status_string", "uzip_version", "uzip_comm_read_staging",
 ]
 
 
@@ -102,6 +102,7 @@ def lib() -> ctypes.CDLL:
             l.uzip_allreduce.argtypes = [vp, vp, sz, i32, i32, vp, vp]
             l.uzip_comm_get_async_error.argtypes = [vp, ctypes.POINTER(i32)]
             l.uzip_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+            l.uzip_comm_read_staging.argtypes = [vp, i32, i32, vp, sz]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
@@ -240,3 +241,106 @@ def status_string(st: int) -> str:
 
 def version() -> str:
     return lib().uzip_version().decode()
+
+
+# ----------------------------------------------------------------------------- communicator
+def make_config(min_compress_bytes=0, staging_bytes=0, pipe_chunk_bytes=0, max_ctas=0, poll_timeout_ms=0,
+                block_symbols=0, chunk_blocks=0, sample_symbols=0, global_table=False) -> Config:
+    return Config(min_compress_bytes, staging_bytes, pipe_chunk_bytes, max_ctas, poll_timeout_ms,
+                  _params(block_symbols, chunk_blocks, sample_symbols, global_table))
+
+
+def torch_bootstrap(group=None):
+    """uzip_allgather_fn over torch.distributed (bootstrap only):
+    all-gathers `bytes_per_rank` opaque bytes from every rank in rank order."""
+    import torch.distributed as dist
+
+    def cb(send, recv, nbytes, ctx):
+        try:
+            world = dist.get_world_size(group)
+            mine = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8)
+            dev = torch.device("cuda", torch.cuda.current_device()) \
+                if dist.get_backend(group) == "nccl" else torch.device("cpu")
+            parts = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(world)]
+            dist.all_gather(parts, mine.to(dev), group=group)
+            blob = torch.cat(parts).cpu().numpy().tobytes()
+            ctypes.memmove(recv, blob, len(blob))
+            return 0
+        except Exception as e:  # pragma: no cover - reported as UZIP_ERR_COMM
+            print(f"uzip bootstrap failed: {e}")
+            return 1
+    return ALLGATHER_FN(cb)
+
+
+class Comm:
+    """One rank's communicator (include/uzip.h uzip_comm_t).  Argument marshalling only."""
+
+    def __init__(self, handle: ctypes.c_void_p, nranks: int, rank: int, device: int, keep=None):
+        self.h = handle
+        self.nranks, self.rank, self.device = nranks, rank, device
+        self._keep = keep
+
+    @classmethod
+    def from_group(cls, group=None, device: int | None = None, **cfg) -> "Comm":
+        """Multi-process init (one process per GPU); torch.distributed bootstraps the IPC handles."""
+        import torch.distributed as dist
+        dev = torch.cuda.current_device() if device is None else device
+        torch.cuda.set_device(dev)
+        cb = torch_bootstrap(group)
+        h = ctypes.c_void_p()
+        c = make_config(**cfg)
+        _check(lib().uzip_comm_init(ctypes.byref(h), dist.get_world_size(group), dist.get_rank(group), dev, cb,
+                                    None, ctypes.byref(c)), "uzip_comm_init")
+        return cls(h, dist.get_world_size(group), dist.get_rank(group), dev, keep=cb)
+
+    @classmethod
+    def init_all(cls, nranks: int, devices=None, **cfg) -> list:
+        """Single-process init of nranks communicators; devices may repeat (loopback on one GPU)."""
+        devices = list(devices) if devices is not None else [torch.cuda.current_device()] * nranks
+        hs = (ctypes.c_void_p * nranks)()
+        ds = (ctypes.c_int * nranks)(*devices)
+        c = make_config(**cfg)
+        _check(lib().uzip_comm_init_all(hs, nranks, ds, ctypes.byref(c)), "uzip_comm_init_all")
+        return [cls(ctypes.c_void_p(hs[r]), nranks, r, devices[r]) for r in range(nranks)]
+
+    def destroy(self):
+        if self.h:
+            _check(lib().uzip_comm_destroy(self.h), "uzip_comm_destroy")
+            self.h = None
+
+    def send(self, t: torch.Tensor, peer: int, stream=None):
+        _check(lib().uzip_send(ctypes.c_void_p(t.data_ptr()), t.numel(), uz_dtype(t.dtype), peer, self.h,
+                               _stream(stream)), "uzip_send")
+
+    def recv(self, t: torch.Tensor, peer: int, stream=None):
+        _check(lib().uzip_recv(ctypes.c_void_p(t.data_ptr()), t.numel(), uz_dtype(t.dtype), peer, self.h,
+                               _stream(stream)), "uzip_recv")
+
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor, stream=None):
+        _check(lib().uzip_allgather(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), inp.numel(),
+                                    uz_dtype(inp.dtype), self.h, _stream(stream)), "uzip_allgather")
+
+    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, stream=None):
+        _check(lib().uzip_reduce_scatter(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                         out.numel(), uz_dtype(inp.dtype), SUM, self.h, _stream(stream)),
+               "uzip_reduce_scatter")
+
+    def all_reduce(self, out: torch.Tensor, inp: torch.Tensor | None = None, stream=None):
+        inp = out if inp is None else inp
+        _check(lib().uzip_allreduce(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), out.numel(),
+                                    uz_dtype(out.dtype), SUM, self.h, _stream(stream)), "uzip_allreduce")
+
+    def async_error(self) -> int:
+        e = ctypes.c_int(0)
+        _check(lib().uzip_comm_get_async_error(self.h, ctypes.byref(e)), "uzip_comm_get_async_error")
+        return e.value
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().uzip_get_stats(self.h, ctypes.byref(s)), "uzip_get_stats")
+        return {"raw_bytes": s.raw_bytes, "wire_bytes": s.wire_bytes, "compressed": bool(s.compressed)}
+
+    def read_staging(self, src: int, slot: int, nbytes: int) -> bytes:
+        buf = ctypes.create_string_buffer(nbytes)
+        _check(lib().uzip_comm_read_staging(self.h, src, slot, buf, nbytes), "uzip_comm_read_staging")
+        return buf.raw

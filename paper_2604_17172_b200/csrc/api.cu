@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 
+#include "plan.h"
 #include "uzip_internal.h"
 
 using namespace uzip;
@@ -56,7 +57,7 @@ size_t uzip_compress_bound(size_t count, uzip_dtype_t dtype, const uzip_codec_pa
 size_t uzip_workspace_bytes(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params) {
   StreamGeom g;
   if (resolve_geom((int)dtype, count, params, &g) != UZIP_OK) return 0;
-  return (size_t)CodecWs::bytes_for(g.n_chunks, g.n_tiles());
+  return (size_t)(64 + EncWs::bytes(g.n_chunks, tiles_of(g)));
 }
 
 uzip_status_t uzip_workspace_init(void *ws, size_t ws_bytes, void *stream) {
@@ -73,8 +74,28 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   if (!out || !ws || !aligned16(out) || !aligned16(ws)) return UZIP_ERR_INVALID_ARG;
   if (count > 0 && (!in || !aligned16(in))) return UZIP_ERR_INVALID_ARG;
   if (out_capacity < g.total(g.n_blocks * (uint64_t)g.B)) return UZIP_ERR_CAPACITY;
-  if (ws_bytes < CodecWs::bytes_for(g.n_chunks, g.n_tiles())) return UZIP_ERR_CAPACITY;
-  cudaError_t e = launch_compress((int)dtype, in, g, out, d_out_bytes, ws, (cudaStream_t)stream, 0);
+  if (ws_bytes < 64 + EncWs::bytes(g.n_chunks, tiles_of(g))) return UZIP_ERR_CAPACITY;
+  // one encode job, one destination (the caller's stream buffer), no flags
+  Plan p;
+  memset(&p, 0, sizeof p);
+  p.dtype = (int)dtype;
+  uint8_t *w = static_cast<uint8_t *>(ws);
+  p.ticket = reinterpret_cast<uint32_t *>(w + 16);
+  p.err = reinterpret_cast<uint32_t *>(w + 24);
+  p.timeout_ns = 10000000000ull;
+  EncJob &J = p.e[0];
+  J.in = static_cast<const uint8_t *>(in);
+  J.g = g;
+  J.ntiles = tiles_of(g);
+  J.nd = 1;
+  J.dst[0] = static_cast<uint8_t *>(out);
+  J.d_out_bytes = d_out_bytes;
+  EncWs::carve(w + 64, g.n_chunks, J.ntiles, J);
+  p.ne = 1;
+  p.n_e_items = J.ntiles;
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaError_t e = launch_tables((int)dtype, p, cs);
+  if (e == cudaSuccess) e = launch_fused((int)dtype, p, cs, 0);
   if (e != cudaSuccess) {
     fprintf(stderr, "uzip_compress: %s\n", cudaGetErrorString(e));
     return UZIP_ERR_CUDA;

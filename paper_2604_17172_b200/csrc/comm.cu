@@ -1,27 +1,557 @@
-// comm.cu -- communicator and fused collectives (filled in next).
+// comm.cu -- communicator and the compressed P2P / collective entry points.
+//
+// Host side only: it lays out the symmetric region every rank exports
+// (staging slots, tile flags, credits), maps the peers' regions (CUDA IPC
+// between processes, direct pointers in single-process mode), and turns each
+// call into rounds of at most one staging slot, each round = k_table + one
+// k_fused launch (fused.cu).  No host synchronization on the data path.
+//
+// Paper: split-send P2P, compress-on-send / decompress-
+// (reduce)-on-receive collectives, two-shot allreduce,
+// selective compression and threshold, bounded staging
+// (P:487-490).  Readings R10-R12 in DESIGN.md.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "plan.h"
 #include "uzip_internal.h"
 
+using namespace uzip;
+
+namespace {
+
+constexpr uint64_t kCtrlBytes = 256;
+constexpr uint32_t kMagic = 0x555A4950u;  // "PIZU"
+
+struct Layout {
+  uint64_t slot_bytes, max_tiles;
+  uint64_t off_credit, off_flags, off_stage, total;
+  void init(int nranks, uint64_t slot) {
+    slot_bytes = round16(slot);
+    max_tiles = slot_bytes / 8192 + 2;
+    off_credit = kCtrlBytes;
+    off_flags = round16(off_credit + 8ull * kMaxRanks * 2);
+    off_stage = (off_flags + 8ull * nranks * 2 * max_tiles + 4095) & ~4095ull;
+    total = off_stage + (uint64_t)nranks * 2 * slot_bytes;
+  }
+  uint64_t credit(int dst, int slot) const { return off_credit + 8ull * (dst * 2 + slot); }
+  uint64_t flags(int src, int slot) const { return off_flags + 8ull * ((uint64_t)(src * 2 + slot) * max_tiles); }
+  uint64_t stage(int src, int slot) const { return off_stage + (uint64_t)(src * 2 + slot) * slot_bytes; }
+};
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+struct uzip_comm {
+  uint32_t magic;
+  int nranks, rank, device;
+  bool ipc;
+  uzip_config_t cfg;
+  Layout L;
+  uint8_t *region;                 // own symmetric region
+  uint8_t *peer[kMaxRanks];        // every rank's region as addressable from here
+  uint32_t send_seq[kMaxRanks];    // rounds sent to / received from each peer (epoch = seq + 1)
+  uint32_t recv_seq[kMaxRanks];
+  uint8_t *ws;                     // local workspace: ticket, done counters, wire counter, encode jobs
+  uint64_t ws_bytes, ws_job_bytes, max_chunks;
+  cudaStream_t side;               // private stream for host reads (async error, stats)
+  uzip_stats_t last;
+  int nested;                      // inside uzip_allreduce: phases accumulate stats
+};
+
+namespace {
+
+uint32_t *ws_ticket(uzip_comm *c) { return reinterpret_cast<uint32_t *>(c->ws); }
+uint32_t *ws_done(uzip_comm *c, int j) { return reinterpret_cast<uint32_t *>(c->ws + 16) + j; }
+unsigned long long *ws_wire(uzip_comm *c) { return reinterpret_cast<unsigned long long *>(c->ws + 64); }
+uint8_t *ws_job(uzip_comm *c, int j) { return c->ws + 128 + (uint64_t)j * c->ws_job_bytes; }
+
+uzip_config_t resolve_cfg(const uzip_config_t *in) {
+  uzip_config_t c;
+  memset(&c, 0, sizeof c);
+  if (in) c = *in;
+  auto env = [](const char *k, uint64_t dflt) -> uint64_t {
+    const char *v = getenv(k);
+    return v ? strtoull(v, nullptr, 0) : dflt;
+  };
+  if (!c.min_compress_bytes) c.min_compress_bytes = env("UZIP_MIN_COMPRESS_BYTES", 1ull << 20);
+  if (c.min_compress_bytes == ~0ull) c.min_compress_bytes = ~0ull;  // never compress
+  if (!c.staging_bytes) c.staging_bytes = env("UZIP_STAGING_BYTES", 512ull << 20);
+  if (!c.pipe_chunk_bytes) c.pipe_chunk_bytes = env("UZIP_PIPE_CHUNK_BYTES", ~0ull);
+  if (!c.max_ctas) c.max_ctas = (uint32_t)env("UZIP_MAX_CTAS", 0);
+  if (!c.poll_timeout_ms) c.poll_timeout_ms = (uint32_t)env("UZIP_POLL_TIMEOUT_MS", 10000);
+  return c;
+}
+
+// Allocate and zero the local region and workspace of a communicator.
+uzip_status_t alloc_local(uzip_comm *c) {
+  if (cudaSetDevice(c->device) != cudaSuccess) return UZIP_ERR_CUDA;
+  c->L.init(c->nranks, c->cfg.staging_bytes / 2);
+  if (cudaMalloc(&c->region, c->L.total) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (cudaMemset(c->region, 0, c->L.off_stage) != cudaSuccess) return UZIP_ERR_CUDA;
+  // workspace sized for the largest round any call can plan (one slot of elements)
+  StreamGeom g;
+  uzip_status_t st = resolve_geom(kBF16, c->L.slot_bytes / 2, &c->cfg.codec, &g);
+  if (st != UZIP_OK) return st;
+  c->max_chunks = g.n_chunks + 1;
+  c->ws_job_bytes = EncWs::bytes(c->max_chunks, g.n_tiles() + 1);
+  c->ws_bytes = 128 + (uint64_t)kMaxRanks * c->ws_job_bytes;
+  if (cudaMalloc(&c->ws, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (cudaMemset(c->ws, 0, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (cudaDeviceSynchronize() != cudaSuccess) return UZIP_ERR_CUDA;
+  return UZIP_OK;
+}
+
+uzip_comm *new_comm(int nranks, int rank, int device, const uzip_config_t *cfg) {
+  uzip_comm *c = new uzip_comm;
+  memset(c, 0, sizeof *c);
+  c->magic = kMagic;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->cfg = resolve_cfg(cfg);
+  return c;
+}
+
+void free_comm(uzip_comm *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->ipc)
+    for (int p = 0; p < c->nranks; ++p)
+      if (p != c->rank && c->peer[p]) cudaIpcCloseMemHandle(c->peer[p]);
+  if (c->region) cudaFree(c->region);
+  if (c->ws) cudaFree(c->ws);
+  if (c->side) cudaStreamDestroy(c->side);
+  c->magic = 0;
+  delete c;
+}
+
+bool valid(uzip_comm *c) { return c && c->magic == kMagic; }
+
+// ---------------------------------------------------------------- round planning
+// Elements per round: the largest multiple of one table chunk (CB*B) whose
+// worst-case stream fits a staging slot; raw rounds fill the slot.
+uint64_t round_elems(uzip_comm *c, int dt, bool compressed, uint64_t count, StreamGeom *g_full) {
+  const uint32_t eb = elem_bytes(dt);
+  if (!compressed) return std::max<uint64_t>(1, std::min<uint64_t>(c->L.slot_bytes, c->cfg.pipe_chunk_bytes) / eb);
+  StreamGeom g;
+  resolve_geom(dt, count, &c->cfg.codec, &g);
+  if (g_full) *g_full = g;
+  const uint64_t unit = g.global ? (uint64_t)g.B : (uint64_t)g.CB * g.B;
+  uint64_t lo = 1, hi = std::min<uint64_t>(c->L.slot_bytes, c->cfg.pipe_chunk_bytes) / eb / unit + 1;
+  while (lo < hi) {  // largest k with bound(k*unit) <= slot and tiles/chunks within the workspace
+    const uint64_t k = (lo + hi + 1) / 2;
+    StreamGeom t;
+    resolve_geom(dt, k * unit, &c->cfg.codec, &t);
+    const bool fits = t.total(t.n_blocks * (uint64_t)t.B) <= c->L.slot_bytes && t.n_tiles() + 1 <= c->L.max_tiles &&
+                      t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_tiles() + 1) <= c->ws_job_bytes;
+    if (fits) lo = k;
+    else hi = k - 1;
+  }
+  return lo * unit;
+}
+
+bool compress_message(uzip_comm *c, uint64_t message_bytes) { return message_bytes >= c->cfg.min_compress_bytes; }
+
+void base_plan(uzip_comm *c, Plan &p, int dt) {
+  memset(&p, 0, sizeof p);
+  p.dtype = dt;
+  p.ticket = ws_ticket(c);
+  p.err = reinterpret_cast<uint32_t *>(c->region);
+  p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
+}
+
+// Encode job of `n` elements at `in` (round stream) into destinations dsts.
+void enc_job(uzip_comm *c, Plan &p, int j, int dt, const uint8_t *in, uint64_t n, bool compressed,
+             const std::vector<int> &dsts) {
+  EncJob &J = p.e[j];
+  memset(&J, 0, sizeof J);
+  J.in = in;
+  J.raw = compressed ? 0 : 1;
+  J.raw_bytes = n * elem_bytes(dt);
+  if (compressed) {
+    resolve_geom(dt, n, &c->cfg.codec, &J.g);
+    J.ntiles = tiles_of(J.g);
+    EncWs::carve(ws_job(c, j), J.g.n_chunks, J.ntiles, J);
+  } else {
+    J.ntiles = std::max<uint64_t>(1, (J.raw_bytes + kRawTileBytes - 1) / kRawTileBytes);
+  }
+  J.nd = (uint32_t)dsts.size();
+  for (size_t i = 0; i < dsts.size(); ++i) {
+    const int d = dsts[i];
+    const uint32_t q = c->send_seq[d]++;
+    const int slot = q & 1;
+    J.dst[i] = c->peer[d] + c->L.stage(c->rank, slot);
+    J.flag[i] = reinterpret_cast<unsigned long long *>(c->peer[d] + c->L.flags(c->rank, slot));
+    J.credit[i] = reinterpret_cast<const unsigned long long *>(c->region + c->L.credit(d, slot));
+    J.epoch[i] = q + 1;
+  }
+  J.wire_acc = ws_wire(c);
+  p.ne = j + 1;
+}
+
+// Decode job: `srcs` in rank order; `me_idx` >= 0 marks the local raw input (reduce).
+void dec_job(uzip_comm *c, Plan &p, int j, int dt, uint64_t n, bool compressed, const std::vector<int> &srcs,
+             int me_idx, const uint8_t *own, uint8_t *out) {
+  DecJob &J = p.d[j];
+  memset(&J, 0, sizeof J);
+  J.raw = compressed ? 0 : 1;
+  J.raw_bytes = n * elem_bytes(dt);
+  if (compressed) {
+    resolve_geom(dt, n, &c->cfg.codec, &J.g);
+    J.ntiles = tiles_of(J.g);
+  } else {
+    J.ntiles = std::max<uint64_t>(1, (J.raw_bytes + kRawTileBytes - 1) / kRawTileBytes);
+  }
+  J.nsrc = (uint32_t)srcs.size();
+  J.me = me_idx;
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    if ((int)i == me_idx) {
+      J.src[i] = own;
+      continue;
+    }
+    const int s = srcs[i];
+    const uint32_t q = c->recv_seq[s]++;
+    const int slot = q & 1;
+    J.src[i] = c->region + c->L.stage(s, slot);
+    J.flag[i] = reinterpret_cast<const unsigned long long *>(c->region + c->L.flags(s, slot));
+    J.credit[i] = reinterpret_cast<unsigned long long *>(c->peer[s] + c->L.credit(c->rank, slot));
+    J.epoch[i] = q + 1;
+  }
+  J.out = out;
+  J.done = ws_done(c, j);
+  p.nd_jobs = j + 1;
+}
+
+uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
+  for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
+  for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += p.d[j].ntiles;
+  p.n_c_items = p.has_copy ? p.c.ntiles : 0;
+  if (compressed && p.ne > 0) {
+    if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;
+  }
+  if (launch_fused(p.dtype, p, st, (int)c->cfg.max_ctas) != cudaSuccess) return UZIP_ERR_CUDA;
+  return UZIP_OK;
+}
+
+std::vector<int> peers_from(uzip_comm *c) {  // rank+1, rank+2, ... (spreads first-hop load)
+  std::vector<int> v;
+  for (int i = 1; i < c->nranks; ++i) v.push_back((c->rank + i) % c->nranks);
+  return v;
+}
+
+// Stats of a call: raw_bytes = bytes this rank would store into peers
+// uncompressed; wire_bytes = bytes it actually stored (device counter for
+// compressed streams).
+uzip_status_t begin_call(uzip_comm *c, uint64_t egress_raw, bool compressed, cudaStream_t st) {
+  if (cudaSetDevice(c->device) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (c->nested) {
+    c->last.raw_bytes += egress_raw;
+    return UZIP_OK;
+  }
+  c->last.raw_bytes = egress_raw;
+  c->last.compressed = compressed ? 1 : 0;
+  c->last.wire_bytes = 0;
+  if (cudaMemsetAsync(ws_wire(c), 0, 8, st) != cudaSuccess) return UZIP_ERR_CUDA;
+  return UZIP_OK;
+}
+
+uzip_status_t check_dtype(uzip_dtype_t dt) {
+  return ((int)dt < 0 || (int)dt > 2) ? UZIP_ERR_UNSUPPORTED_DTYPE : UZIP_OK;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
 extern "C" {
-uzip_status_t uzip_comm_init(uzip_comm_t *, int, int, int, uzip_allgather_fn, void *, const uzip_config_t *) {
-  return UZIP_ERR_NOT_IMPLEMENTED;
+
+uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_device, uzip_allgather_fn bootstrap,
+                             void *ctx, const uzip_config_t *cfg) {
+  if (!comm || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !bootstrap)
+    return UZIP_ERR_INVALID_ARG;
+  *comm = nullptr;
+  uzip_comm *c = new_comm(nranks, rank, cuda_device, cfg);
+  c->ipc = true;
+  uzip_status_t st = alloc_local(c);
+  if (st != UZIP_OK) {
+    free_comm(c);
+    return st;
+  }
+  struct Card {
+    cudaIpcMemHandle_t h;
+    uint64_t total, slot, max_tiles;
+    int32_t device, rank;
+  } mine, all[kMaxRanks];
+  memset(&mine, 0, sizeof mine);
+  if (cudaIpcGetMemHandle(&mine.h, c->region) != cudaSuccess) {
+    free_comm(c);
+    return UZIP_ERR_CUDA;
+  }
+  mine.total = c->L.total;
+  mine.slot = c->L.slot_bytes;
+  mine.max_tiles = c->L.max_tiles;
+  mine.device = cuda_device;
+  mine.rank = rank;
+  if (bootstrap(&mine, all, sizeof(Card), ctx) != 0) {
+    free_comm(c);
+    return UZIP_ERR_COMM;
+  }
+  for (int p = 0; p < nranks; ++p) {
+    if (all[p].rank != p || all[p].slot != mine.slot || all[p].total != mine.total) {
+      free_comm(c);
+      return UZIP_ERR_COMM;  // every rank must use the same configuration
+    }
+    if (p == rank) {
+      c->peer[p] = c->region;
+      continue;
+    }
+    void *ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[p].h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "uzip_comm_init: rank %d cannot map rank %d: %s\n", rank, p, cudaGetErrorString(e));
+      free_comm(c);
+      return UZIP_ERR_COMM;
+    }
+    c->peer[p] = static_cast<uint8_t *>(ptr);
+  }
+  int dummy = 0, sink[kMaxRanks];
+  if (bootstrap(&dummy, sink, sizeof(int), ctx) != 0) {  // everyone mapped everyone
+    free_comm(c);
+    return UZIP_ERR_COMM;
+  }
+  *comm = c;
+  return UZIP_OK;
 }
-uzip_status_t uzip_comm_init_all(uzip_comm_t *, int, const int *, const uzip_config_t *) {
-  return UZIP_ERR_NOT_IMPLEMENTED;
+
+uzip_status_t uzip_comm_init_all(uzip_comm_t *comms, int nranks, const int *devices, const uzip_config_t *cfg) {
+  if (!comms || !devices || nranks < 1 || nranks > kMaxRanks) return UZIP_ERR_INVALID_ARG;
+  std::vector<uzip_comm *> cs(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    cs[r] = new_comm(nranks, r, devices[r], cfg);
+    uzip_status_t st = alloc_local(cs[r]);
+    if (st != UZIP_OK) {
+      for (auto *c : cs) free_comm(c);
+      return st;
+    }
+  }
+  for (int r = 0; r < nranks; ++r) {
+    cudaSetDevice(devices[r]);
+    for (int p = 0; p < nranks; ++p) {
+      cs[r]->peer[p] = cs[p]->region;
+      if (devices[p] != devices[r]) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(devices[p], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          for (auto *c : cs) free_comm(c);
+          return UZIP_ERR_CUDA;
+        }
+        cudaGetLastError();
+      }
+    }
+  }
+  for (int r = 0; r < nranks; ++r) comms[r] = cs[r];
+  return UZIP_OK;
 }
-uzip_status_t uzip_comm_destroy(uzip_comm_t) { return UZIP_ERR_NOT_IMPLEMENTED; }
-uzip_status_t uzip_send(const void *, size_t, uzip_dtype_t, int, uzip_comm_t, void *) {
-  return UZIP_ERR_NOT_IMPLEMENTED;
+
+uzip_status_t uzip_comm_destroy(uzip_comm_t comm) {
+  if (!valid(comm)) return UZIP_ERR_INVALID_ARG;
+  cudaSetDevice(comm->device);
+  cudaDeviceSynchronize();
+  free_comm(comm);
+  return UZIP_OK;
 }
-uzip_status_t uzip_recv(void *, size_t, uzip_dtype_t, int, uzip_comm_t, void *) { return UZIP_ERR_NOT_IMPLEMENTED; }
-uzip_status_t uzip_allgather(const void *, void *, size_t, uzip_dtype_t, uzip_comm_t, void *) {
-  return UZIP_ERR_NOT_IMPLEMENTED;
+
+uzip_status_t uzip_send(const void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t c, void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (peer < 0 || peer >= c->nranks || peer == c->rank) return UZIP_ERR_INVALID_ARG;
+  if (count == 0) return UZIP_OK;
+  if (!buf || !aligned16(buf)) return UZIP_ERR_INVALID_ARG;
+  const int dt = (int)dtype;
+  const uint32_t eb = elem_bytes(dt);
+  const bool comp = compress_message(c, count * eb);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (uzip_status_t s = begin_call(c, count * eb, comp, st)) return s;
+  const uint64_t per = round_elems(c, dt, comp, count, nullptr);
+  for (uint64_t o = 0; o < count; o += per) {
+    const uint64_t n = std::min<uint64_t>(per, count - o);
+    Plan p;
+    base_plan(c, p, dt);
+    enc_job(c, p, 0, dt, static_cast<const uint8_t *>(buf) + o * eb, n, comp, {peer});
+    if (uzip_status_t s = launch(c, p, comp, st)) return s;
+  }
+  return UZIP_OK;
 }
-uzip_status_t uzip_reduce_scatter(const void *, void *, size_t, uzip_dtype_t, uzip_op_t, uzip_comm_t, void *) {
-  return UZIP_ERR_NOT_IMPLEMENTED;
+
+uzip_status_t uzip_recv(void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t c, void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (peer < 0 || peer >= c->nranks || peer == c->rank) return UZIP_ERR_INVALID_ARG;
+  if (count == 0) return UZIP_OK;
+  if (!buf || !aligned16(buf)) return UZIP_ERR_INVALID_ARG;
+  const int dt = (int)dtype;
+  const uint32_t eb = elem_bytes(dt);
+  const bool comp = compress_message(c, count * eb);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (uzip_status_t s = begin_call(c, 0, comp, st)) return s;
+  const uint64_t per = round_elems(c, dt, comp, count, nullptr);
+  for (uint64_t o = 0; o < count; o += per) {
+    const uint64_t n = std::min<uint64_t>(per, count - o);
+    Plan p;
+    base_plan(c, p, dt);
+    dec_job(c, p, 0, dt, n, comp, {peer}, -1, nullptr, static_cast<uint8_t *>(buf) + o * eb);
+    if (uzip_status_t s = launch(c, p, comp, st)) return s;
+  }
+  return UZIP_OK;
 }
-uzip_status_t uzip_allreduce(const void *, void *, size_t, uzip_dtype_t, uzip_op_t, uzip_comm_t, void *) {
-  return UZIP_ERR_NOT_IMPLEMENTED;
+
+uzip_status_t uzip_allgather(const void *sendbuf, void *recvbuf, size_t sendcount, uzip_dtype_t dtype,
+                             uzip_comm_t c, void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (sendcount == 0) return UZIP_OK;
+  if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
+  const int dt = (int)dtype;
+  const uint32_t eb = elem_bytes(dt);
+  const int N = c->nranks, me = c->rank;
+  const uint64_t msg = (uint64_t)N * sendcount * eb;  // R10: the user message (total output)
+  const bool comp = N > 1 && compress_message(c, msg);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (uzip_status_t s = begin_call(c, (uint64_t)(N - 1) * sendcount * eb, comp, st)) return s;
+  const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
+  uint8_t *out = static_cast<uint8_t *>(recvbuf);
+  const bool in_place = in == out + (uint64_t)me * sendcount * eb;
+  const uint64_t per = round_elems(c, dt, comp, sendcount, nullptr);
+  const std::vector<int> peers = peers_from(c);
+  for (uint64_t o = 0; o < sendcount; o += per) {
+    const uint64_t n = std::min<uint64_t>(per, sendcount - o);
+    Plan p;
+    base_plan(c, p, dt);
+    if (N > 1) enc_job(c, p, 0, dt, in + o * eb, n, comp, peers);  // one stream, fanned out (a10)
+    int j = 0;
+    for (int s : peers) {
+      dec_job(c, p, j, dt, n, comp, {s}, -1, nullptr, out + ((uint64_t)s * sendcount + o) * eb);
+      ++j;
+    }
+    if (!in_place) {
+      p.has_copy = 1;
+      p.c.src = in + o * eb;
+      p.c.dst = out + ((uint64_t)me * sendcount + o) * eb;
+      p.c.bytes = n * eb;
+      p.c.ntiles = (p.c.bytes + kRawTileBytes - 1) / kRawTileBytes;
+    }
+    if (uzip_status_t s = launch(c, p, comp, st)) return s;
+  }
+  return UZIP_OK;
 }
-uzip_status_t uzip_comm_get_async_error(uzip_comm_t, uzip_status_t *) { return UZIP_ERR_NOT_IMPLEMENTED; }
-uzip_status_t uzip_get_stats(uzip_comm_t, uzip_stats_t *) { return UZIP_ERR_NOT_IMPLEMENTED; }
+
+uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t recvcount, uzip_dtype_t dtype,
+                                  uzip_op_t op, uzip_comm_t c, void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (op != UZIP_SUM) return UZIP_ERR_INVALID_ARG;
+  if (recvcount == 0) return UZIP_OK;
+  if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
+  const int dt = (int)dtype;
+  const uint32_t eb = elem_bytes(dt);
+  const int N = c->nranks, me = c->rank;
+  const uint64_t msg = (uint64_t)N * recvcount * eb;  // R10: the user message (total input)
+  const bool comp = compress_message(c, msg);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (uzip_status_t s = begin_call(c, (uint64_t)(N - 1) * recvcount * eb, comp, st)) return s;
+  const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
+  uint8_t *out = static_cast<uint8_t *>(recvbuf);
+  const uint64_t per = round_elems(c, dt, comp, recvcount, nullptr);
+  const std::vector<int> peers = peers_from(c);
+  std::vector<int> all;
+  for (int r = 0; r < N; ++r) all.push_back(r);
+  for (uint64_t o = 0; o < recvcount; o += per) {
+    const uint64_t n = std::min<uint64_t>(per, recvcount - o);
+    Plan p;
+    base_plan(c, p, dt);
+    int j = 0;
+    for (int d : peers) {  // shard d of my input -> its owner; my own shard is never compressed
+      enc_job(c, p, j, dt, in + ((uint64_t)d * recvcount + o) * eb, n, comp, {d});
+      ++j;
+    }
+    if (N == 1) {
+      p.has_copy = in + o * eb != out + o * eb;
+      p.c.src = in + o * eb;
+      p.c.dst = out + o * eb;
+      p.c.bytes = n * eb;
+      p.c.ntiles = (p.c.bytes + kRawTileBytes - 1) / kRawTileBytes;
+    } else {
+      dec_job(c, p, 0, dt, n, comp, all, me, in + ((uint64_t)me * recvcount + o) * eb, out + o * eb);
+    }
+    if (uzip_status_t s = launch(c, p, comp, st)) return s;
+  }
+  return UZIP_OK;
 }
+
+uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype, uzip_op_t op,
+                             uzip_comm_t c, void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (op != UZIP_SUM) return UZIP_ERR_INVALID_ARG;
+  if (count == 0) return UZIP_OK;
+  const int N = c->nranks;
+  if (count % (size_t)N != 0) return UZIP_ERR_INVALID_ARG;
+  if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
+  const uint32_t eb = elem_bytes((int)dtype);
+  const uint64_t shard = count / N;
+  if ((shard * eb) % 16 != 0 && N > 1) return UZIP_ERR_INVALID_ARG;  // shards stay 16-byte aligned
+  // Two-shot: reduce-scatter into my shard of recvbuf, then
+  // allgather of the reduced shards, each phase compressing once (R12).  The
+  // threshold applies to the user message (R10) in both phases.
+  const uint64_t saved = c->cfg.min_compress_bytes;
+  const bool comp = compress_message(c, count * eb);
+  uzip_status_t s = begin_call(c, 0, comp, (cudaStream_t)stream);
+  if (s != UZIP_OK) return s;
+  c->cfg.min_compress_bytes = comp ? 0 : ~0ull;
+  c->nested = 1;
+  uint8_t *mine = static_cast<uint8_t *>(recvbuf) + (uint64_t)c->rank * shard * eb;
+  s = uzip_reduce_scatter(sendbuf, mine, shard, dtype, op, c, stream);
+  if (s == UZIP_OK && N > 1) s = uzip_allgather(mine, recvbuf, shard, dtype, c, stream);
+  c->nested = 0;
+  c->cfg.min_compress_bytes = saved;
+  return s;
+}
+
+uzip_status_t uzip_comm_get_async_error(uzip_comm_t c, uzip_status_t *err) {
+  if (!valid(c) || !err) return UZIP_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  uint32_t v = 0;
+  if (cudaMemcpyAsync(&v, c->region, 4, cudaMemcpyDeviceToHost, c->side) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (cudaStreamSynchronize(c->side) != cudaSuccess) return UZIP_ERR_CUDA;
+  *err = (uzip_status_t)v;
+  return UZIP_OK;
+}
+
+uzip_status_t uzip_comm_read_staging(uzip_comm_t c, int src, int slot, void *host, size_t bytes) {
+  if (!valid(c) || src < 0 || src >= c->nranks || src == c->rank || (slot & ~1) || !host) return UZIP_ERR_INVALID_ARG;
+  if (bytes > c->L.slot_bytes) return UZIP_ERR_CAPACITY;
+  cudaSetDevice(c->device);
+  if (cudaMemcpyAsync(host, c->region + c->L.stage(src, slot), bytes, cudaMemcpyDeviceToHost, c->side) != cudaSuccess)
+    return UZIP_ERR_CUDA;
+  return cudaStreamSynchronize(c->side) == cudaSuccess ? UZIP_OK : UZIP_ERR_CUDA;
+}
+
+uzip_status_t uzip_get_stats(uzip_comm_t c, uzip_stats_t *out) {
+  if (!valid(c) || !out) return UZIP_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  unsigned long long w = 0;
+  if (cudaMemcpyAsync(&w, ws_wire(c), 8, cudaMemcpyDeviceToHost, c->side) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (cudaStreamSynchronize(c->side) != cudaSuccess) return UZIP_ERR_CUDA;
+  *out = c->last;
+  out->wire_bytes = c->last.compressed ? w : c->last.raw_bytes;
+  return UZIP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1051 @@
+// fused.cu -- the Uzip hot path for sm_100a: table build and ONE persistent
+// kernel per launch that encodes, transfers, decodes and reduces.
+//
+//   k_table  a2+a3  sampled per-chunk histogram ("the first 256 KB" of each
+//                   chunk) -> rule-N1 frequencies (R5) -> encode
+//                   reciprocals; one launch covers every stream of a call.
+//   k_fused  E items  a1+a4+a5+a6: split (the residual leaves for every
+//                   destination as soon as it is split: split-send),
+//                   warp-per-block 32-lane rANS,
+//                   decoupled look-back so each block is stored once at its
+//                   final offset (Step 3 removed), stores straight
+//                   into the destinations' staging, tile flag
+//                   release (a12).
+//            C items  plain copies (own allgather shard).
+//            D items  a7+a8(+a9): acquire a tile flag, decode (table-driven),
+//                   join; with several sources, decode each and fold in rank
+//                   order in fp32 before one rounding (R11).
+//
+// Stream bytes equal the CPU oracle's (tests/test_gpu_codec.py,
+// tests/test_gpu_comm.py); layout in DESIGN.md section 2.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdio>
+
+#include "plan.h"
+#include "uzip_internal.h"
+
+namespace uzip {
+
+// ================================================================ k_table
+// grid = (max n_chunks, ne), kTabThreads threads: one CTA per chunk histograms
+// the chunk's sample ("the first 256 KB") with warp-aggregated shared
+// atomics, normalizes (rule N1, R5) and writes the chunk's encode entries and
+// 512-byte serialized table.  No cross-CTA scratch: nothing to reset.
+constexpr int kTabThreads = 512;
+constexpr int kTabWarps = kTabThreads / 32;
+
+template <int DT>
+__global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ Plan P) {
+  __shared__ uint32_t hist[kTabWarps][256];
+  __shared__ uint32_t cnt[256];
+  __shared__ unsigned long long red64[8];
+  __shared__ uint32_t red32[8];
+
+  const EncJob &J = P.e[blockIdx.y];
+  if (J.raw) return;
+  const StreamGeom &g = J.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t c = blockIdx.x;
+
+  // reset the look-back words of this job for the k_fused launch that follows
+  for (uint64_t t = (uint64_t)blockIdx.x * kTabThreads + tid; t < tiles_of(g); t += (uint64_t)gridDim.x * kTabThreads)
+    J.tile_status[t] = 0ull;
+  if (c >= g.n_chunks) return;
+
+  for (int i = tid; i < kTabWarps * 256; i += kTabThreads) (&hist[0][0])[i] = 0;
+  __syncthreads();
+
+  const uint32_t len = g.sample_len(c);
+  constexpr uint32_t kPer = (DT == kF32) ? 4 : 8;  // symbols per 16-byte vector
+  constexpr int kUnroll = 8;
+  const uint8_t *base = J.in + (uint64_t)c * g.CB * g.B * elem_bytes(DT);
+  const uint32_t nvec = len / kPer;
+  for (uint32_t v0 = 0; v0 < nvec; v0 += kTabThreads * kUnroll) {
+    uint4 w[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t v = v0 + u * kTabThreads + tid;
+      w[u] = v < nvec ? ldg_nc_v4(base + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const bool ok = v0 + u * kTabThreads + tid < nvec;
+      uint32_t s_lo, s_hi = 0;
+      if (DT == kBF16) {
+        uint32_t r;
+        split4_bf16(w[u].x, w[u].y, s_lo, r);
+        split4_bf16(w[u].z, w[u].w, s_hi, r);
+      } else if (DT == kF16) {
+        uint32_t r;
+        split4_f16(w[u].x, w[u].y, s_lo, r);
+        split4_f16(w[u].z, w[u].w, s_hi, r);
+      } else {
+        uint2 lo;
+        uint32_t hi;
+        split4_f32(w[u], s_lo, lo, hi);
+      }
+      // warp-aggregated increments: the lanes holding the same symbol add once
+#pragma unroll
+      for (int k = 0; k < (int)kPer; ++k) {
+        const uint32_t s = ok ? ((k < 4 ? s_lo : s_hi) >> (8 * (k & 3))) & 0xFFu : 0x100u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, s);
+        if (s < 256 && (uint32_t)lane == (uint32_t)(__ffs(peers) - 1))
+          atomicAdd(&hist[warp][s], (uint32_t)__popc(peers));
+      }
+    }
+  }
+  for (uint32_t i = nvec * kPer + tid; i < len; i += kTabThreads) {  // sample length not a vector multiple
+    uint32_t s;
+    if (DT == kF32) s = (reinterpret_cast<const uint32_t *>(base)[i] >> 23) & 0xFFu;
+    else if (DT == kBF16) s = (reinterpret_cast<const uint16_t *>(base)[i] >> 7) & 0xFFu;
+    else s = reinterpret_cast<const uint16_t *>(base)[i] >> 8;
+    atomicAdd(&hist[warp][s], 1u);
+  }
+  __syncthreads();
+  if (tid >= 256) return;  // 8 warps normalize
+
+  // ---- rule N1 (R5)
+  {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < kTabWarps; ++w) sum += hist[w][tid];
+    cnt[tid] = sum;
+  }
+  // total and argmax (lowest symbol on ties): key = cnt<<8 | (255 - s)
+  unsigned long long key = ((unsigned long long)cnt[tid] << 8) | (255u - tid);
+  unsigned long long tot = cnt[tid];
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long ok = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+    key = ok > key ? ok : key;
+    tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+  }
+  if (lane == 0) {
+    red64[warp] = key;
+    red32[warp] = (uint32_t)tot;
+  }
+  asm volatile("bar.sync 1, 256;");
+  unsigned long long best_key = 0, total = 0;
+  for (int w = 0; w < 8; ++w) {
+    best_key = red64[w] > best_key ? red64[w] : best_key;
+    total += red32[w];
+  }
+  const uint32_t best = 255u - (uint32_t)(best_key & 0xFFu);
+  uint32_t f;
+  if (total == 0) f = kM / 256;
+  else f = 1u + (uint32_t)(((unsigned long long)cnt[tid] * (kM - 256)) / total);
+  asm volatile("bar.sync 1, 256;");
+  uint32_t fs = f;
+  for (int o = 16; o; o >>= 1) fs += __shfl_xor_sync(0xFFFFFFFFu, fs, o);
+  if (lane == 0) red32[warp] = fs;
+  asm volatile("bar.sync 1, 256;");
+  uint32_t fsum = 0;
+  for (int w = 0; w < 8; ++w) fsum += red32[w];
+  if (total != 0 && tid == (int)best) f += kM - fsum;
+  asm volatile("bar.sync 1, 256;");
+  uint32_t incl = f;  // exclusive prefix (cdf) over 256 symbols
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) red32[warp] = incl;
+  asm volatile("bar.sync 1, 256;");
+  uint32_t woff = 0;
+  for (int w = 0; w < warp; ++w) woff += red32[w];
+  const uint32_t cdf = woff + incl - f;
+  J.enc[c * 256 + tid] = make_enc_entry(f, cdf);
+  J.tab16[c * 256 + tid] = (uint16_t)f;
+}
+
+// ================================================================ shared pieces
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagInc = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void raise_err(const Plan &P, uint32_t code) { atomicCAS(P.err, 0u, code); }
+
+// Poll a tile flag until its epoch matches (thread-level; bounded by the
+// plan's timeout, aborts when another CTA raised an error).
+__device__ bool wait_flag(const Plan &P, const unsigned long long *f, uint32_t epoch, unsigned long long &v) {
+  unsigned long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    v = ld_acquire_sys_u64(f);
+    if ((uint32_t)(v >> 32) == epoch) return true;
+    if ((spin & 63) == 63) {
+      if (ld_volatile_u32(P.err)) return false;
+      const unsigned long long now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > P.timeout_ns) {
+        raise_err(P, UZIP_ERR_TIMEOUT);
+        return false;
+      }
+    }
+    __nanosleep(32);
+  }
+}
+
+// Credit: the destination consumed epoch-2 from this slot (a12).
+__device__ bool wait_credit(const Plan &P, const unsigned long long *cr, uint32_t epoch) {
+  if (!cr || epoch <= 2) return true;
+  unsigned long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    if (ld_acquire_sys_u64(cr) >= (unsigned long long)(epoch - 2)) return true;
+    if ((spin & 63) == 63) {
+      if (ld_volatile_u32(P.err)) return false;
+      const unsigned long long now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > P.timeout_ns) {
+        raise_err(P, UZIP_ERR_TIMEOUT);
+        return false;
+      }
+    }
+    __nanosleep(64);
+  }
+}
+
+// Decoupled look-back (one full warp) over the tiles of one stream; returns
+// the exclusive prefix of tile t, or ~0 on abort.
+__device__ unsigned long long lookback(const Plan &P, unsigned long long *status, uint64_t t,
+                                       unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) {
+    if (lane == 0) st_relaxed_u64(&status[0], kFlagInc | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed_u64(&status[t], kFlagAgg | agg);
+  unsigned long long excl = 0, t0 = 0;
+  int64_t base = (int64_t)t - 1;
+  for (int spin = 0;; ++spin) {
+    const int64_t idx = base - lane;
+    unsigned long long s = idx >= 0 ? ld_relaxed_u64(&status[idx]) : (kFlagInc | 0ull);
+    const uint32_t flag = (uint32_t)(s >> 62);
+    const uint32_t inc = __ballot_sync(0xFFFFFFFFu, flag == 2);
+    const uint32_t notready = __ballot_sync(0xFFFFFFFFu, flag == 0);
+    const int first_inc = inc ? __ffs(inc) - 1 : 31;
+    const uint32_t needed = first_inc == 31 ? 0xFFFFFFFFu : ((2u << first_inc) - 1u);
+    if (notready & needed) {
+      if ((spin & 255) == 255) {
+        bool stop = false;
+        if (lane == 0) {
+          const unsigned long long now = globaltimer_ns();
+          if (ld_volatile_u32(P.err)) stop = true;
+          else if (t0 == 0) t0 = now;
+          else if (now - t0 > P.timeout_ns) {
+            raise_err(P, UZIP_ERR_TIMEOUT);
+            stop = true;
+          }
+        }
+        if (__shfl_sync(0xFFFFFFFFu, stop, 0)) return ~0ull;
+      }
+      __nanosleep(32);
+      continue;
+    }
+    excl += warp_sum_u64(lane <= first_inc ? (s & kValMask) : 0ull);
+    if (inc) break;
+    base -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(&status[t], kFlagInc | (excl + agg));
+  return excl;
+}
+
+// Directory entry -> payload bytes of a block; flags entries no encoder emits.
+__device__ __forceinline__ uint32_t block_size(uint32_t d, uint32_t B, bool &bad) {
+  if (d == kRawBlock) return B;
+  if (d >= B / 2) {
+    bad = true;
+    return B;
+  }
+  const uint32_t sz = (uint32_t)round16(128 + 2ull * d);
+  if (sz >= B) bad = true;
+  return sz;
+}
+
+// Decode table of one chunk: f:12 <<20 | (slot-cdf):12 <<8 | sym:8 (a7).
+// All 256 threads; returns false (uniformly) if the table is invalid.
+__device__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t f = ld_cg_u16(ft + tid);
+  uint32_t incl = f;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += tt;
+  }
+  const uint32_t anyzero = __ballot_sync(0xFFFFFFFFu, f == 0);
+  if (lane == 31) s_red[warp] = incl | (anyzero ? 0x80000000u : 0u);
+  __syncthreads();
+  uint32_t woff = 0, fsum = 0, bad = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t v = s_red[w];
+    bad |= v >> 31;
+    if (w < warp) woff += v & 0x7FFFFFFFu;
+    fsum += v & 0x7FFFFFFFu;
+  }
+  __syncthreads();
+  if (fsum != kM || bad) return false;
+  const uint32_t cdf = woff + incl - f;
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t fk = __shfl_sync(0xFFFFFFFFu, f, k);
+    const uint32_t ck = __shfl_sync(0xFFFFFFFFu, cdf, k);
+    const uint32_t sk = (uint32_t)(warp * 32 + k);
+    for (uint32_t t = lane; t < fk; t += 32) dtab[ck + t] = (fk << 20) | (t << 8) | sk;
+  }
+  return true;
+}
+
+// a8: one warp decodes the K-word block in `pay` (smem) into 8-bit symbols.
+// Returns false if the block is corrupt (word overrun, end state != L).
+template <int B>
+__device__ __forceinline__ bool rans_decode_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
+                                                 uint8_t *symb) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t *pay32 = reinterpret_cast<const uint32_t *>(pay);
+  const uint16_t *pay16 = reinterpret_cast<const uint16_t *>(pay);
+  uint32_t x = pay32[lane];
+  int32_t p = (int32_t)K;
+  bool bad = false;
+#pragma unroll 4
+  for (uint32_t j = 0; j < (uint32_t)(B / 32); ++j) {
+    const uint32_t e = dtab[x & (kM - 1)];
+    symb[j * 32 + lane] = (uint8_t)e;
+    x = (e >> 20) * (x >> kProbBits) + ((e >> 8) & 0xFFFu);
+    const bool need = x < kL;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
+    const int32_t k = __popc(m);
+    if (k > p) {
+      bad = true;
+      break;
+    }
+    if (need) x = (x << 16) | pay16[64 + p - k + __popc(m & lt)];
+    p -= k;
+  }
+  return !(bad || p != 0 || __any_sync(0xFFFFFFFFu, x != kL));
+}
+
+// Join 8-bit symbols (smem) with the residual plane(s) of block b; stores B
+// elements of DT at dst (128-bit stores).
+template <int DT, int B>
+__device__ __forceinline__ void join_block(const uint8_t *syms, const uint8_t *stream, const StreamGeom &g,
+                                           uint64_t b, uint8_t *dst) {
+  const int lane = threadIdx.x & 31;
+  if (DT == kF32) {
+#pragma unroll 4
+    for (uint32_t e = lane * 4; e < (uint32_t)B; e += 128) {
+      const uint32_t s4 = *reinterpret_cast<const uint32_t *>(syms + e);
+      const uint2 lo = ld_cg_v2(stream + g.off_res0 + 2 * (b * B + e));
+      const uint32_t h4 = ld_cg_u32c(stream + g.off_res1 + b * B + e);
+      *reinterpret_cast<uint4 *>(dst + 4 * e) = join4_f32(s4, lo, h4);
+    }
+  } else {
+#pragma unroll 4
+    for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
+      const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
+      const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
+      uint4 o;
+      if (DT == kBF16) {
+        join4_bf16(s8.x, r8.x, o.x, o.y);
+        join4_bf16(s8.y, r8.y, o.z, o.w);
+      } else {
+        join4_f16(s8.x, r8.x, o.x, o.y);
+        join4_f16(s8.y, r8.y, o.z, o.w);
+      }
+      *reinterpret_cast<uint4 *>(dst + 2 * e) = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fp32 fold helpers (a9, R11)
+template <int DT>
+__device__ __forceinline__ float widen(uint32_t bits) {
+  if (DT == kBF16) return __uint_as_float(bits << 16);
+  if (DT == kF16) return __half2float(__ushort_as_half((unsigned short)bits));
+  return __uint_as_float(bits);
+}
+template <int DT>
+__device__ __forceinline__ uint32_t narrow(float v) {
+  if (v != v) return DT == kF32 ? 0x7FFFFFFFu : 0x7FFFu;  // canonical NaN
+  if (DT == kBF16) return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+  if (DT == kF16) return (uint32_t)__half_as_ushort(__float2half_rn(v));
+  return __float_as_uint(v);
+}
+__device__ __forceinline__ float fold(float acc, float x, bool first) { return first ? x : __fadd_rn(acc, x); }
+
+// Fold 16 bytes of elements into acc[0..kPer) (kPer = 8 for 2-byte types, 4 for fp32).
+template <int DT>
+__device__ __forceinline__ void fold_vec(float *acc, uint4 v, bool first) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if (DT == kF32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = fold(acc[i], widen<DT>(w[i]), first);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] = fold(acc[2 * i], widen<DT>(w[i] & 0xFFFFu), first);
+      acc[2 * i + 1] = fold(acc[2 * i + 1], widen<DT>(w[i] >> 16), first);
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ uint4 narrow_vec(const float *acc) {
+  uint4 o;
+  uint32_t *w = &o.x;
+  if (DT == kF32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = narrow<DT>(acc[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = narrow<DT>(acc[2 * i]) | (narrow<DT>(acc[2 * i + 1]) << 16);
+  }
+  return o;
+}
+
+// ================================================================ k_fused
+template <int DT, int B>
+struct FusedCfg {
+  static constexpr int kVec = (DT == kF32) ? 4 : 8;        // elements per 16-byte load
+  static constexpr int kIters = B / (32 * kVec);            // loads per lane per block
+  static constexpr int kBatch = kIters < 16 ? kIters : 16;
+  static constexpr int kRounds = B / 32;
+  static constexpr int kEncTab = 4096;                      // 256 x uint4
+  static constexpr int kWarpBuf = 2 * B;                    // two B-byte buffers per warp
+  static constexpr int kDecTab = 4096 * 4;
+  static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce)
+  static constexpr int smem(bool dec, bool red) {
+    return kEncTab + kWarps * kWarpBuf + (dec ? kDecTab : 0) + (red ? kWarps * kAcc : 0);
+  }
+};
+
+struct FusedShared {
+  uint32_t ticket;
+  uint32_t abort;
+  uint32_t size[kWarps], k[kWarps];
+  unsigned long long prefix;
+  unsigned long long src_off[kMaxRanks];
+  unsigned long long src_payload[kMaxRanks];
+  uint32_t red[kWarps];
+  uint32_t credit_ok;
+};
+
+// ---------------------------------------------------------------- E item
+template <int DT, int B>
+__device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &enc_key) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    uint32_t ok = 1;
+    if (!((S.credit_ok >> jidx) & 1u)) {
+      for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
+      if (ok) S.credit_ok |= 1u << jidx;
+    }
+    S.abort = ok ? 0u : 1u;
+  }
+  __syncthreads();
+  if (S.abort) return;
+
+  if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256) {
+      const uint4 v = ldg_nc_v4(J.in + o0 + 16 * i);
+      for (uint32_t d = 0; d < J.nd; ++d) *reinterpret_cast<uint4 *>(J.dst[d] + o0 + 16 * i) = v;
+    }
+    for (uint64_t i = nv * 16 + tid; i < len; i += 256) {
+      const uint8_t v = J.in[o0 + i];
+      for (uint32_t d = 0; d < J.nd; ++d) J.dst[d][o0 + i] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      for (uint32_t d = 0; d < J.nd; ++d)
+        if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
+    }
+    return;
+  }
+
+  const StreamGeom &g = J.g;
+  uint4 *tab = reinterpret_cast<uint4 *>(smem);
+  uint8_t *sym = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint8_t *blk = sym + B;
+  uint16_t *blk16 = reinterpret_cast<uint16_t *>(blk);
+  uint32_t *blk32 = reinterpret_cast<uint32_t *>(blk);
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t key = ((uint64_t)jidx << 48) | c;
+  if (g.n_blocks && key != enc_key) {
+    tab[tid] = J.enc[c * 256 + tid];
+    enc_key = key;
+  }
+  __syncthreads();
+
+  const uint64_t b = b0 + warp;
+  uint32_t K = 0, size = 0;
+  if (b < g.n_blocks) {
+    // ---- a1: split; the residual goes straight to every destination (split-send)
+    const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
+#pragma unroll
+    for (int h = 0; h < C::kIters; h += C::kBatch) {
+      uint4 v[C::kBatch];
+#pragma unroll
+      for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
+#pragma unroll
+      for (int i = 0; i < C::kBatch; ++i) {
+        const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;
+        if (DT == kF32) {
+          uint32_t s4, h4;
+          uint2 lo;
+          split4_f32(v[i], s4, lo, h4);
+          *reinterpret_cast<uint32_t *>(sym + e) = s4;
+          for (uint32_t d = 0; d < J.nd; ++d) {
+            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
+            *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
+          }
+        } else {
+          uint32_t s0, s1, r0, r1;
+          if (DT == kBF16) {
+            split4_bf16(v[i].x, v[i].y, s0, r0);
+            split4_bf16(v[i].z, v[i].w, s1, r1);
+          } else {
+            split4_f16(v[i].x, v[i].y, s0, r0);
+            split4_f16(v[i].z, v[i].w, s1, r1);
+          }
+          *reinterpret_cast<uint2 *>(sym + e) = make_uint2(s0, s1);
+          for (uint32_t d = 0; d < J.nd; ++d)
+            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(r0, r1);
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- a4: 32 interleaved rANS lanes, rounds R-1 .. 0
+    const uint32_t lt = lanemask_lt();
+    uint32_t x = kL;
+    uint32_t wp = 0;
+    constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
+#pragma unroll 4
+    for (int j = C::kRounds - 1; j >= 0; --j) {
+      const uint32_t s = sym[j * 32 + lane];
+      const uint4 e = tab[s];
+      const bool p = (x | 0x7FFFFu) >= e.y;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+      if (p) {
+        const uint32_t idx = wp + __popc(m & lt);
+        if (idx < kCap) blk16[64 + idx] = (uint16_t)x;
+        x >>= 16;
+      }
+      wp += __popc(m);
+      const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
+      x = x + e.z + q * e.w;
+    }
+    K = wp;
+    const uint32_t coded = (uint32_t)round16(128 + 2ull * K);
+    if (coded >= (uint32_t)B) {
+      size = B;  // stored raw (R13)
+    } else {
+      size = coded;
+      blk32[lane] = x;
+      const uint32_t pad_words = (coded - 128 - 2 * K) / 2;
+      if ((uint32_t)lane < pad_words) blk16[64 + K + lane] = 0;
+    }
+  }
+  if (lane == 0) {
+    S.size[warp] = size;
+    S.k[warp] = (size == (uint32_t)B) ? kRawBlock : K;
+  }
+  __syncthreads();
+
+  // ---- a5: tile prefix by decoupled look-back
+  if (warp == 0) {
+    unsigned long long agg = lane < kWarps ? S.size[lane] : 0u;
+    agg = warp_sum_u64(agg);
+    const unsigned long long excl = lookback(P, J.tile_status, t, agg);
+    if (lane == 0) S.prefix = excl;
+  }
+  __syncthreads();
+  if (S.prefix == ~0ull) return;  // aborted (timeout / peer error)
+
+  if (b < g.n_blocks) {
+    unsigned long long off = S.prefix;
+    for (int w = 0; w < warp; ++w) off += S.size[w];
+    const uint4 *srcv = reinterpret_cast<const uint4 *>(size == (uint32_t)B ? sym : blk);
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      uint8_t *o = J.dst[d];
+      if (lane == 0) {
+        reinterpret_cast<uint32_t *>(o + g.off_dir)[b] = S.k[warp];
+        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(o + g.off_coff)[b / g.CB] = off;
+      }
+      uint4 *dstv = reinterpret_cast<uint4 *>(o + g.off_pay + off);
+      for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
+    }
+  }
+  // the chunk's first tile carries its serialized table (the receiver waits for it)
+  if (g.n_blocks && b0 % g.CB == 0 && tid < 32) {
+    const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[tid];
+    for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[tid] = v;
+  }
+  if (t == J.ntiles - 1) {  // ---- last tile: header (sizes before/after), pads, raw tail
+    unsigned long long payload = S.prefix;
+    for (int w = 0; w < kWarps; ++w) payload += S.size[w];
+    const uint64_t total = g.total(payload);
+    if (tid == 0) {
+      uint32_t h[16];
+      for (int i = 0; i < 16; ++i) h[i] = 0;
+      h[0] = 0x31425A55u;  // "UZB1"
+      h[1] = kVersion | (g.dtype << 16) | ((g.global & 1u) << 24);
+      h[2] = (uint32_t)g.n;
+      h[3] = (uint32_t)(g.n >> 32);
+      h[4] = g.B;
+      h[5] = g.CB;
+      h[6] = g.S;
+      h[7] = kProbBits | (kLanes << 8) | (kLBits << 16);
+      h[8] = (uint32_t)g.n_blocks;
+      h[9] = (uint32_t)g.n_chunks;
+      h[10] = (uint32_t)payload;
+      h[11] = (uint32_t)(payload >> 32);
+      h[12] = (uint32_t)total;
+      h[13] = (uint32_t)(total >> 32);
+      for (uint32_t d = 0; d < J.nd; ++d) {
+        uint4 *o = reinterpret_cast<uint4 *>(J.dst[d]);
+        for (int i = 0; i < 4; ++i) o[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+      }
+      if (J.d_out_bytes) *J.d_out_bytes = total;
+      if (J.wire_acc) atomicAdd(J.wire_acc, (unsigned long long)total * J.nd);
+    }
+    const uint64_t e1 = g.off_coff + 8 * g.n_chunks, e2 = g.off_dir + 4 * g.n_blocks;
+    const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+    const uint8_t *tsrc = J.in + g.n_coded * g.eb;
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      uint8_t *o = J.dst[d];
+      for (uint64_t p = e1 + tid; p < g.off_dir; p += 256) o[p] = 0;
+      for (uint64_t p = e2 + tid; p < g.off_pay; p += 256) o[p] = 0;
+      uint8_t *tdst = o + g.off_tail(payload);
+      for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    bool any = false;
+    for (uint32_t d = 0; d < J.nd; ++d) any |= J.flag[d] != nullptr;
+    if (any) {
+      __threadfence_system();
+      const unsigned long long off16 = S.prefix >> 4;
+      for (uint32_t d = 0; d < J.nd; ++d)
+        if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- C item
+__device__ void copy_item(const CopyJob &Cj, uint64_t t) {
+  const uint64_t o0 = t * kRawTileBytes;
+  const uint64_t len = min((uint64_t)kRawTileBytes, Cj.bytes - o0);
+  const uint64_t nv = len / 16;
+  for (uint64_t i = threadIdx.x; i < nv; i += 256)
+    *reinterpret_cast<uint4 *>(Cj.dst + o0 + 16 * i) = ldg_nc_v4(Cj.src + o0 + 16 * i);
+  for (uint64_t i = nv * 16 + threadIdx.x; i < len; i += 256) Cj.dst[o0 + i] = Cj.src[o0 + i];
+}
+
+// Completion of one D item: the last tile of the job releases the sources' slots.
+__device__ void dec_done(const DecJob &J) {
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  const uint32_t old = atomicAdd(J.done, 1u);
+  if (old == (uint32_t)J.ntiles - 1) {
+    __threadfence();
+    *J.done = 0;
+    for (uint32_t s = 0; s < J.nsrc; ++s)
+      if ((int32_t)s != J.me && J.credit[s]) st_release_sys_u64(J.credit[s], (unsigned long long)J.epoch[s]);
+  }
+}
+
+// Thread 0: acquire tile t of source s (and the chunk's first tile, which
+// carries the table, when the table is not cached).  Sets S.abort on failure.
+__device__ void acquire_tile(const Plan &P, const DecJob &J, uint32_t s, uint64_t t, bool need_table,
+                             FusedShared &S) {
+  unsigned long long v = 0;
+  bool ok = wait_flag(P, J.flag[s] + t, J.epoch[s], v);
+  S.src_off[s] = (v & 0xFFFFFFFFull) << 4;
+  if (ok && need_table && !J.raw && J.g.n_blocks) {
+    const uint64_t first = (t * kTileBlocks / J.g.CB) * J.g.CB / kTileBlocks;
+    if (first != t) {
+      unsigned long long v2;
+      ok = wait_flag(P, J.flag[s] + first, J.epoch[s], v2);
+    }
+  }
+  S.abort = ok ? 0u : 1u;
+}
+
+// Per-block payload offsets within a tile from the directory (all lanes of a warp).
+__device__ __forceinline__ void tile_block(const uint8_t *stream, const StreamGeom &g, uint64_t b0, int warp,
+                                           unsigned long long tile_off, uint32_t &K, unsigned long long &off,
+                                           unsigned long long &tile_end, bool &bad) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t *dir = reinterpret_cast<const uint32_t *>(stream + g.off_dir);
+  uint32_t d = 0, sz = 0;
+  bool bb = false;
+  if (lane < kWarps && b0 + lane < g.n_blocks) {
+    d = ld_cg_u32c(dir + b0 + lane);
+    sz = block_size(d, g.B, bb);
+  }
+  bad = __any_sync(0xFFFFFFFFu, bb);
+  uint32_t incl = sz;
+  for (int o = 1; o < 8; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  K = __shfl_sync(0xFFFFFFFFu, d, warp);
+  off = tile_off + __shfl_sync(0xFFFFFFFFu, incl - sz, warp);
+  tile_end = tile_off + __shfl_sync(0xFFFFFFFFu, incl, kWarps - 1);
+}
+
+// Stage block payload into smem (warp).
+__device__ __forceinline__ void stage_payload(const uint8_t *stream, const StreamGeom &g, unsigned long long off,
+                                              uint32_t size, uint8_t *pay) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t *p = stream + g.off_pay + off;
+  for (uint32_t i = lane; i < size / 16; i += 32) reinterpret_cast<uint4 *>(pay)[i] = ld_cg_v4(p + 16 * i);
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- D item: decode (+ join)
+template <int DT, int B>
+__device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &dec_key) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const StreamGeom &g = J.g;
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t key = (1ull << 63) | ((uint64_t)jidx << 48) | c;
+  const bool need_table = key != dec_key;
+  if (tid == 0) acquire_tile(P, J, 0, t, need_table, S);
+  __syncthreads();
+  if (S.abort) return;
+  const uint8_t *stream = J.src[0];
+  if (J.raw) {
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256)
+      *reinterpret_cast<uint4 *>(J.out + o0 + 16 * i) = ld_cg_v4(stream + o0 + 16 * i);
+    for (uint64_t i = nv * 16 + tid; i < len; i += 256) J.out[o0 + i] = stream[o0 + i];
+    __syncthreads();
+    dec_done(J);
+    return;
+  }
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf);
+  if (g.n_blocks && need_table) {
+    if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
+      if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+      dec_key = ~0ull;
+      return;
+    }
+    dec_key = key;
+  }
+  __syncthreads();
+  uint8_t *pay = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint8_t *symb = pay + B;
+  const uint64_t b = b0 + warp;
+  uint32_t K;
+  unsigned long long off, tile_end;
+  bool bad;
+  tile_block(stream, g, b0, warp, S.src_off[0], K, off, tile_end, bad);
+  if (b < g.n_blocks && !bad) {
+    const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
+    stage_payload(stream, g, off, size, pay);
+    const uint8_t *syms = pay;
+    if (K != kRawBlock) {
+      if (!rans_decode_warp<B>(pay, K, dtab, symb)) bad = true;
+      syms = symb;
+    }
+    __syncwarp();
+    if (!bad) join_block<DT, B>(syms, stream, g, b, J.out + b * (uint64_t)B * g.eb);
+  }
+  if (bad && (threadIdx.x & 31) == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+  if (t == J.ntiles - 1) {  // raw tail
+    const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+    const uint8_t *tsrc = stream + g.off_tail(tile_end);
+    uint8_t *tdst = J.out + g.n_coded * g.eb;
+    for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
+  }
+  __syncthreads();
+  dec_done(J);
+}
+
+// ---------------------------------------------------------------- D item: decode + reduce (a9)
+template <int DT, int B>
+__device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &dec_key) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const StreamGeom &g = J.g;
+  const uint32_t eb = elem_bytes(DT);
+  constexpr int kPer = C::kVec;
+
+  if (J.raw) {  // ---- below the threshold: fold raw tiles
+    for (uint32_t s = 0; s < J.nsrc; ++s) {
+      if ((int32_t)s == J.me) continue;
+      if (tid == 0) acquire_tile(P, J, s, t, false, S);
+      __syncthreads();
+      if (S.abort) return;
+    }
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256) {
+      float acc[8];
+      for (uint32_t s = 0; s < J.nsrc; ++s) {
+        const uint8_t *p = J.src[s] + o0 + 16 * i;
+        const uint4 v = ((int32_t)s == J.me) ? ldg_nc_v4(p) : ld_cg_v4(p);
+        fold_vec<DT>(acc, v, s == 0);
+      }
+      *reinterpret_cast<uint4 *>(J.out + o0 + 16 * i) = narrow_vec<DT>(acc);
+    }
+    for (uint64_t i = nv * 16 / eb + tid; i < len / eb; i += 256) {  // scalar tail
+      float acc = 0.f;
+      for (uint32_t s = 0; s < J.nsrc; ++s) {
+        const uint8_t *p = J.src[s] + o0 + i * eb;
+        const uint32_t bits = DT == kF32 ? *reinterpret_cast<const uint32_t *>(p)
+                                         : (uint32_t)*reinterpret_cast<const uint16_t *>(p);
+        acc = fold(acc, widen<DT>(bits), s == 0);
+      }
+      const uint32_t r = narrow<DT>(acc);
+      if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + o0 + i * eb) = r;
+      else *reinterpret_cast<uint16_t *>(J.out + o0 + i * eb) = (uint16_t)r;
+    }
+    __syncthreads();
+    dec_done(J);
+    return;
+  }
+
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t b = b0 + warp;
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf);
+  float *acc = reinterpret_cast<float *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::kDecTab) + warp * B;
+  uint8_t *pay = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint8_t *symb = pay + B;
+  bool bad = false;
+
+  for (uint32_t s = 0; s < J.nsrc; ++s) {
+    const bool first = s == 0;
+    if ((int32_t)s == J.me) {  // own shard: never compressed
+      if (b < g.n_blocks) {
+        const uint8_t *src = J.src[s] + b * (uint64_t)B * eb;
+        for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer) {
+          float a[8];
+          if (!first)
+            for (int i = 0; i < kPer; ++i) a[i] = acc[e + i];
+          fold_vec<DT>(a, ldg_nc_v4(src + e * eb), first);
+          for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
+        }
+      }
+      continue;
+    }
+    const uint64_t key = (2ull << 62) | ((uint64_t)jidx << 48) | ((uint64_t)s << 40) | c;
+    const bool need_table = key != dec_key;
+    if (tid == 0) acquire_tile(P, J, s, t, need_table, S);
+    __syncthreads();
+    if (S.abort) return;
+    const uint8_t *stream = J.src[s];
+    if (g.n_blocks && need_table) {
+      if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
+        if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+        dec_key = ~0ull;
+        return;
+      }
+      dec_key = key;
+    }
+    __syncthreads();
+    uint32_t K;
+    unsigned long long off, tile_end;
+    bool tb;
+    tile_block(stream, g, b0, warp, S.src_off[s], K, off, tile_end, tb);
+    bad |= tb;
+    if (tid == 0) S.src_payload[s] = tile_end;
+    if (b < g.n_blocks && !tb) {
+      const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
+      stage_payload(stream, g, off, size, pay);
+      const uint8_t *syms = pay;
+      if (K != kRawBlock) {
+        if (!rans_decode_warp<B>(pay, K, dtab, symb)) bad = true;
+        syms = symb;
+      }
+      __syncwarp();
+      // join + fold 8 (fp32: 4) elements per lane step
+      for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer) {
+        uint4 v;
+        if (DT == kF32) {
+          const uint32_t s4 = *reinterpret_cast<const uint32_t *>(syms + e);
+          const uint2 lo = ld_cg_v2(stream + g.off_res0 + 2 * (b * B + e));
+          const uint32_t h4 = ld_cg_u32c(stream + g.off_res1 + b * B + e);
+          v = join4_f32(s4, lo, h4);
+        } else {
+          const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
+          const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
+          if (DT == kBF16) {
+            join4_bf16(s8.x, r8.x, v.x, v.y);
+            join4_bf16(s8.y, r8.y, v.z, v.w);
+          } else {
+            join4_f16(s8.x, r8.x, v.x, v.y);
+            join4_f16(s8.y, r8.y, v.z, v.w);
+          }
+        }
+        float a[8];
+        if (!first)
+          for (int i = 0; i < kPer; ++i) a[i] = acc[e + i];
+        fold_vec<DT>(a, v, first);
+        for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
+      }
+    }
+    __syncwarp();
+  }
+  if (bad && lane == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+  if (b < g.n_blocks) {  // one rounding to the dtype, 128-bit stores
+    uint8_t *dst = J.out + b * (uint64_t)B * eb;
+    for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer)
+      *reinterpret_cast<uint4 *>(dst + e * eb) = narrow_vec<DT>(acc + e);
+  }
+  __syncthreads();
+  if (t == J.ntiles - 1) {  // raw tails of every source, folded in rank order
+    const uint64_t tail = g.n - g.n_coded;
+    for (uint64_t i = tid; i < tail; i += 256) {
+      float a = 0.f;
+      for (uint32_t s = 0; s < J.nsrc; ++s) {
+        const uint8_t *p = ((int32_t)s == J.me) ? J.src[s] + (g.n_coded + i) * eb
+                                                : J.src[s] + g.off_tail(S.src_payload[s]) + i * eb;
+        const uint32_t bits = DT == kF32 ? *reinterpret_cast<const uint32_t *>(p)
+                                         : (uint32_t)*reinterpret_cast<const uint16_t *>(p);
+        a = fold(a, widen<DT>(bits), s == 0);
+      }
+      const uint32_t r = narrow<DT>(a);
+      if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + (g.n_coded + i) * eb) = r;
+      else *reinterpret_cast<uint16_t *>(J.out + (g.n_coded + i) * eb) = (uint16_t)r;
+    }
+  }
+  __syncthreads();
+  dec_done(J);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int DT, int B, bool RED>
+__global__ void __launch_bounds__(256, RED ? 1 : 2) k_fused(const __grid_constant__ Plan P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ FusedShared S;
+  const int tid = threadIdx.x;
+  uint64_t enc_key = ~0ull, dec_key = ~0ull;
+  if (tid == 0) S.credit_ok = 0;
+  const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
+  while (true) {
+    if (tid == 0) S.ticket = atomicAdd(P.ticket, 1u);
+    __syncthreads();
+    const uint64_t it = S.ticket;
+    __syncthreads();
+    if (it >= total) break;
+    if (it < ne) {
+      const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key);
+    } else if (it < ne + nc) {
+      copy_item(P.c, it - ne);
+    } else {
+      uint64_t k = it - ne - nc;  // job-major over the decode jobs
+      int j = 0;
+      while (j + 1 < P.nd_jobs && k >= P.d[j].ntiles) k -= P.d[j++].ntiles;
+      if (RED && P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
+      else dec_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {  // the last CTA out resets the ticket for the next launch
+    __threadfence();
+    if (atomicAdd(P.ticket + 1, 1u) == gridDim.x - 1) {
+      P.ticket[0] = 0;
+      P.ticket[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ================================================================ launchers
+namespace {
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int DT>
+cudaError_t launch_tables_t(const Plan &p, cudaStream_t st) {
+  uint64_t max_chunks = 1;  // >= 1: the look-back words are reset even without chunks
+  for (int j = 0; j < p.ne; ++j)
+    if (!p.e[j].raw) max_chunks = p.e[j].g.n_chunks > max_chunks ? p.e[j].g.n_chunks : max_chunks;
+  dim3 grid((unsigned)max_chunks, (unsigned)p.ne);
+  k_table<DT><<<grid, kTabThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, int B, bool RED>
+cudaError_t launch_fused_t(const Plan &p, cudaStream_t st, int max_ctas) {
+  using C = FusedCfg<DT, B>;
+  const bool dec = p.n_d_items > 0;
+  const int smem = C::smem(dec || RED, RED);
+  auto kern = k_fused<DT, B, RED>;
+  static int attr_set = 0;
+  if (attr_set < smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(true, RED));
+    attr_set = C::smem(true, RED);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  if (occ <= 0) occ = 1;
+  const uint64_t items = p.n_e_items + p.n_c_items + p.n_d_items;
+  int grid = sm_count() * occ;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if ((uint64_t)grid > items) grid = (int)(items ? items : 1);
+  kern<<<grid, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, bool RED>
+cudaError_t launch_fused_b(const Plan &p, uint32_t B, cudaStream_t st, int max_ctas) {
+  switch (B) {
+    case 1024: return launch_fused_t<DT, 1024, RED>(p, st, max_ctas);
+    case 2048: return launch_fused_t<DT, 2048, RED>(p, st, max_ctas);
+    default: return launch_fused_t<DT, 4096, RED>(p, st, max_ctas);
+  }
+}
+}  // namespace
+
+cudaError_t launch_tables(int dtype, const Plan &p, cudaStream_t st) {
+  if (p.ne == 0) return cudaSuccess;
+  switch (dtype) {
+    case kBF16: return launch_tables_t<kBF16>(p, st);
+    case kF16: return launch_tables_t<kF16>(p, st);
+    default: return launch_tables_t<kF32>(p, st);
+  }
+}
+
+cudaError_t launch_fused(int dtype, const Plan &p, cudaStream_t st, int max_ctas) {
+  uint32_t B = 4096;
+  bool red = false;
+  for (int j = 0; j < p.ne; ++j)
+    if (!p.e[j].raw) B = p.e[j].g.B;
+  for (int j = 0; j < p.nd_jobs; ++j) {
+    if (!p.d[j].raw) B = p.d[j].g.B;
+    red |= p.d[j].nsrc > 1;
+  }
+  switch (dtype) {
+    case kBF16: return red ? launch_fused_b<kBF16, true>(p, B, st, max_ctas) : launch_fused_b<kBF16, false>(p, B, st, max_ctas);
+    case kF16: return red ? launch_fused_b<kF16, true>(p, B, st, max_ctas) : launch_fused_b<kF16, false>(p, B, st, max_ctas);
+    default: return red ? launch_fused_b<kF32, true>(p, B, st, max_ctas) : launch_fused_b<kF32, false>(p, B, st, max_ctas);
+  }
+}
+
+}  // namespace uzip

@@ -1,0 +1,105 @@
+// plan.h -- work description of one launch of the fused codec/communication
+// kernel (fused.cu).  Shared by the host planners (api.cu, comm.cu) and the
+// device code.
+//
+// A launch processes a ticket space [E items][C items][D items]:
+//   E  encode one tile (8 blocks) of a UZB1 stream and store it into nd
+//      destinations (local stream buffer for uzip_compress, or peers' staging
+//      slots over NVLink for the collectives: "directly write the compressed
+//      data into the communication buffer"), then release a tile
+//      flag in each destination (a12).  Raw mode (below the threshold)
+//      copies 64 KiB raw tiles instead.
+//   C  plain copy tiles (the own shard of an allgather).
+//   D  wait for a tile flag, decode the tile (a7-a8) and join into the output;
+//      with nsrc > 1 it decodes the same tile from every source and folds them
+//      in rank order in fp32 (a9, reading R11) -- decompress before reduce
+//      (P:387-392).
+#pragma once
+
+#include "uzip_device.cuh"
+
+namespace uzip {
+
+constexpr int kMaxRanks = 8;
+constexpr uint32_t kRawTileBytes = 64u << 10;
+
+// Tiles (kTileBlocks blocks each) of a stream; a stream without whole blocks
+// still has one tile (header + raw tail).
+__host__ __device__ inline uint64_t tiles_of(const StreamGeom &g) {
+  const uint64_t t = g.n_tiles();
+  return t ? t : 1;
+}
+
+struct EncJob {
+  const uint8_t *in;                        // local input of this stream
+  StreamGeom g;                             // geometry (compressed mode)
+  uint64_t raw_bytes;                       // raw mode: message bytes
+  uint64_t ntiles;                          // >= 1
+  uint32_t raw;                             // 1 = raw (uncoded) tiles
+  uint32_t nd;                              // destinations
+  uint8_t *dst[kMaxRanks];                  // stream base at each destination
+  unsigned long long *flag[kMaxRanks];      // tile flags at each destination (null: no flags)
+  const unsigned long long *credit[kMaxRanks];  // local word: last epoch the destination consumed from this slot
+  uint32_t epoch[kMaxRanks];                // flag epoch per destination (round sequence + 1)
+  uint4 *enc;                               // per-chunk encode entries (k_table)
+  uint16_t *tab16;                          // per-chunk serialized tables (k_table)
+  unsigned long long *tile_status;          // look-back words (zeroed by k_table)
+  uint64_t *d_out_bytes;                    // codec: stream size (may be null)
+  unsigned long long *wire_acc;             // comm: += stream bytes x nd (may be null)
+};
+
+struct DecJob {
+  StreamGeom g;
+  uint64_t raw_bytes;
+  uint64_t ntiles;
+  uint32_t raw;
+  uint32_t nsrc;                            // 1: plain decode; > 1: decode + reduce over sources
+  int32_t me;                               // reduce: index of the local (uncompressed) source, -1 none
+  uint32_t pad_;
+  const uint8_t *src[kMaxRanks];            // stream base in local staging (me: local raw input)
+  const unsigned long long *flag[kMaxRanks];  // local tile flags per source
+  unsigned long long *credit[kMaxRanks];    // word at the source to release when the round is consumed
+  uint32_t epoch[kMaxRanks];
+  uint8_t *out;                             // output of this stream / shard
+  uint32_t *done;                           // tiles finished (self-resetting counter in ws)
+};
+
+struct CopyJob {
+  const uint8_t *src;
+  uint8_t *dst;
+  uint64_t bytes;
+  uint64_t ntiles;
+};
+
+struct Plan {
+  int32_t ne, nd_jobs, has_copy, dtype;
+  EncJob e[kMaxRanks];
+  DecJob d[kMaxRanks];
+  CopyJob c;
+  uint64_t n_e_items, n_c_items, n_d_items;
+  uint32_t *ticket;                         // self-resetting ticket + exit counter (2 words)
+  uint32_t *err;                            // sticky async error word
+  uint64_t timeout_ns;
+};
+
+// Workspace of one encode job: enc entries, serialized tables, look-back
+// words (all written by k_table before use: no state survives a launch, so
+// the layout may change from call to call).
+struct EncWs {
+  static uint64_t bytes(uint64_t n_chunks, uint64_t n_tiles) {
+    return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * n_tiles);
+  }
+  static void carve(uint8_t *p, uint64_t n_chunks, uint64_t n_tiles, EncJob &j) {
+    (void)n_tiles;
+    j.enc = reinterpret_cast<uint4 *>(p);
+    p += round16(4096 * n_chunks);
+    j.tab16 = reinterpret_cast<uint16_t *>(p);
+    p += round16(512 * n_chunks);
+    j.tile_status = reinterpret_cast<unsigned long long *>(p);
+  }
+};
+
+cudaError_t launch_tables(int dtype, const Plan &p, cudaStream_t st);
+cudaError_t launch_fused(int dtype, const Plan &p, cudaStream_t st, int max_ctas);
+
+}  // namespace uzip

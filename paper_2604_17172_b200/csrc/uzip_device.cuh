@@ -23,7 +23,6 @@ constexpr uint32_t kVersion = 1;
 constexpr int kWarps = 8;                       // warps per CTA in the codec kernels
 constexpr uint32_t kTileBlocks = kWarps;        // blocks per look-back tile
 constexpr uint32_t kMaxB = 4096;                // largest block the GPU kernels stage in smem
-constexpr uint32_t kHistSymsPerCta = 16384;     // sampled symbols per k_table CTA
 
 enum Dtype : int { kBF16 = 0, kF16 = 1, kF32 = 2 };
 
@@ -144,6 +143,52 @@ __device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t *p) {
   uint32_t r;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
   return r;
+}
+__device__ __forceinline__ uint4 ld_cg_v4(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_cg_v2(const void *p) {
+  uint2 r;
+  asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_cg_u32c(const void *p) {
+  uint32_t r;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint16_t ld_cg_u16(const void *p) {
+  uint16_t r;
+  asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+// Cross-GPU flag protocol (a12): payload stores, then a system-scope release
+// of the flag in the consumer's memory; the consumer polls with acquire.
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+  unsigned long long r;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
+  uint32_t r;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t r;

@@ -7,8 +7,6 @@
 
 namespace uzip {
 
-cudaError_t launch_compress(int dtype, const void *in, const StreamGeom &g, void *out, uint64_t *d_out_bytes,
-                            void *ws, cudaStream_t st, int max_ctas);
 cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void *out, uint64_t n, void *ws,
                               int32_t *d_status, cudaStream_t st, int max_ctas);
 

@@ -1,0 +1,249 @@
+"""GPU parity of the fused communication path against the CPU oracle, through the C ABI.
+
+Several ranks run on ONE GPU (uzip_comm_init_all with repeated devices; each
+rank has its own stream and a bounded CTA count so all ranks' persistent
+kernels are co-resident).  The kernels, flags, credits and staging layout are
+the same ones the multi-process NVLink path uses; only the peer pointers differ
+(direct instead of CUDA-IPC-mapped).
+
+Bit-exact checks (0 ulp): P2P recv == send; allgather == concatenation;
+reduce-scatter / allreduce == the oracle's fixed-order fp32 fold (R11);
+the UZB1 stream that lands in the receiver's staging == oracle.compress of the
+round's input (wire-stream parity); compression on vs off
+gives identical outputs; multi-round messages (bounded staging,
+credits) and sub-threshold raw paths; NaN/Inf/denormal/-0 inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+BF16, F16, F32 = 0, 1, 2
+TD = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32}
+VIEW = {BF16: torch.int16, F16: torch.int16, F32: torch.int32}
+NPU = {BF16: np.uint16, F16: np.uint16, F32: np.uint32}
+
+
+@pytest.fixture(scope="module")
+def uz():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_17172_b200 as uz
+    uz.build()
+    return uz
+
+
+def dev(bits, dtype):
+    t = torch.from_numpy(np.ascontiguousarray(bits).view(np.int32 if dtype == F32 else np.int16).copy())
+    return t.view(TD[dtype]).cuda()
+
+
+def host(t, dtype):
+    return t.view(VIEW[dtype]).cpu().numpy().view(NPU[dtype])
+
+
+def gen(dist, n, seed, dtype):
+    if dist == "W":
+        return synth.normal(n, 0.02, seed, dtype)
+    if dist == "special":
+        return synth.special_mix(n, seed, dtype)
+    if dist == "U":
+        return synth.uniform(n, seed, dtype)
+    raise ValueError(dist)
+
+
+class Group:
+    """N loopback ranks on cuda:0, one stream each."""
+
+    def __init__(self, uz, n, **cfg):
+        cfg.setdefault("max_ctas", max(8, 96 // n))
+        cfg.setdefault("poll_timeout_ms", 8000)
+        self.comms = uz.Comm.init_all(n, **cfg)
+        self.streams = [torch.cuda.Stream() for _ in range(n)]
+        self.n = n
+
+    def run(self, fn):
+        torch.cuda.synchronize()
+        for r, c in enumerate(self.comms):
+            with torch.cuda.stream(self.streams[r]):
+                fn(r, c, self.streams[r])
+        torch.cuda.synchronize()
+        errs = [c.async_error() for c in self.comms]
+        assert errs == [0] * self.n, errs
+
+    def close(self):
+        for c in self.comms:
+            c.destroy()
+
+
+CFG_SMALL = dict(staging_bytes=8 << 20, min_compress_bytes=1)  # 4 MiB slots: multi-round messages
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("n", [1, 4095, 3 * 4096 + 17, 300 * 1024 + 5, 3 * (1 << 20) + 77])
+def test_p2p_bit_exact(uz, dtype, n):
+    g = Group(uz, 2, **CFG_SMALL)
+    try:
+        bits = gen("W", n, 11 + n, dtype)
+        x = dev(bits, dtype)
+        y = torch.full_like(x, 7)
+
+        def step(r, c, s):
+            if r == 0:
+                c.send(x, 1, s)
+            else:
+                c.recv(y, 0, s)
+        g.run(step)
+        assert np.array_equal(host(y, dtype), bits)
+        st = g.comms[0].stats()
+        assert st["compressed"] and st["raw_bytes"] == n * (4 if dtype == F32 else 2)
+    finally:
+        g.close()
+
+
+def test_p2p_wire_stream_equals_oracle(uz, orc):
+    """The bytes that land in the receiver's staging are the oracle's UZB1 stream."""
+    g = Group(uz, 2, staging_bytes=64 << 20, min_compress_bytes=1)
+    try:
+        n = 5 * (1 << 20) + 123
+        bits = synth.weights(n, 5)
+        x = dev(bits, BF16)
+        y = torch.empty_like(x)
+        g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else c.recv(y, 0, s))
+        ref = orc.compress(BF16, bits)
+        wire = g.comms[1].read_staging(0, 0, len(ref))
+        assert wire == ref
+        st = g.comms[0].stats()
+        assert st["wire_bytes"] == len(ref)
+        assert np.array_equal(host(y, BF16), bits)
+    finally:
+        g.close()
+
+
+def test_p2p_many_rounds_and_credits(uz, orc):
+    """A message of 7 rounds through 2 slots, repeated: exercises credit waits and epochs."""
+    g = Group(uz, 2, staging_bytes=4 << 20, min_compress_bytes=1)
+    try:
+        n = 7 * (1 << 20) + 9
+        for it in range(3):
+            bits = synth.weights(n, 100 + it)
+            x = dev(bits, BF16)
+            y = torch.empty_like(x)
+            g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else c.recv(y, 0, s))
+            assert np.array_equal(host(y, BF16), bits), it
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("nr", [2, 3, 4])
+@pytest.mark.parametrize("dtype", [BF16, F32])
+@pytest.mark.parametrize("dist", ["W", "special"])
+def test_allgather(uz, nr, dtype, dist):
+    g = Group(uz, nr, **CFG_SMALL)
+    try:
+        n = 2 * (1 << 20) + 4096 * 3 + 5 if dtype == BF16 else (1 << 20) + 77
+        ins = [gen(dist, n, 1000 * r + 3, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(nr * n, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_gather(outs[r], xs[r], s))
+        ref = np.concatenate(ins)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], dtype), ref), r
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("nr", [2, 3, 4])
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+def test_reduce_scatter(uz, orc, nr, dtype):
+    g = Group(uz, nr, **CFG_SMALL)
+    try:
+        m = (1 << 20) + 4096 * 2 + 3  # per-rank shard (ragged tail)
+        ins = [gen("W", nr * m, 77 + r, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.reduce_scatter(outs[r], xs[r], s))
+        ref = orc.reduce_scatter(dtype, ins, nr)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], dtype), ref[r]), r
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("nr", [2, 4])
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("dist", ["W", "special"])
+def test_allreduce(uz, orc, nr, dtype, dist):
+    g = Group(uz, nr, **CFG_SMALL)
+    try:
+        n = nr * ((1 << 20) + 4096 + 8)
+        ins = [gen(dist, n, 500 + r, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(n, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_reduce(outs[r], xs[r], s))
+        ref = orc.allreduce(dtype, ins)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], dtype), ref), r
+    finally:
+        g.close()
+
+
+def test_allreduce_in_place_and_transparency(uz, orc):
+    """In-place allreduce; compressed and uncompressed paths give identical bits."""
+    nr, n = 4, 4 * (600 * 1024)
+    ins = [synth.activations(n // 4096, 40 + r) for r in range(nr)]
+    results = {}
+    for mode, cfg in (("on", dict(min_compress_bytes=1)), ("off", dict(min_compress_bytes=(1 << 64) - 1))):
+        g = Group(uz, nr, staging_bytes=16 << 20, **cfg)
+        try:
+            xs = [dev(b, BF16) for b in ins]
+            g.run(lambda r, c, s: c.all_reduce(xs[r], None, s))
+            results[mode] = [host(x, BF16) for x in xs]
+            assert g.comms[0].stats()["compressed"] == (mode == "on")
+        finally:
+            g.close()
+    ref = orc.allreduce(BF16, ins)
+    for r in range(nr):
+        assert np.array_equal(results["on"][r], ref)
+        assert np.array_equal(results["off"][r], ref)
+
+
+def test_below_threshold_raw_path(uz, orc):
+    """Messages under min_compress_bytes move raw, same results."""
+    nr = 2
+    g = Group(uz, nr, staging_bytes=4 << 20)  # default threshold 1 MiB
+    try:
+        n = 1000 * 2 + 2  # < 1 MiB
+        ins = [synth.weights(n, 9 + r) for r in range(nr)]
+        xs = [dev(b, BF16) for b in ins]
+        outs = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_reduce(outs[r], xs[r], s))
+        ref = orc.allreduce(BF16, ins)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], BF16), ref)
+        st = g.comms[0].stats()
+        assert not st["compressed"] and st["wire_bytes"] == st["raw_bytes"]
+    finally:
+        g.close()
+
+
+def test_mixed_sequence_epochs(uz, orc):
+    """P2P and collectives interleaved on the same channels keep their epochs in step."""
+    nr = 3
+    g = Group(uz, nr, **CFG_SMALL)
+    try:
+        n = (1 << 20) + 11
+        a = [synth.weights(n, 900 + r) for r in range(nr)]
+        xs = [dev(b, BF16) for b in a]
+        ys = [torch.empty(nr * n, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+        p = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        for it in range(2):
+            g.run(lambda r, c, s: c.send(xs[0], 2, s) if r == 0 else (c.recv(p, 0, s) if r == 2 else None))
+            assert np.array_equal(host(p, BF16), a[0])
+            g.run(lambda r, c, s: c.all_gather(ys[r], xs[r], s))
+            for r in range(nr):
+                assert np.array_equal(host(ys[r], BF16), np.concatenate(a))
+    finally:
+        g.close()
