@@ -1,0 +1,140 @@
+"""bench_dist.py -- the N > 1 leg of bench.py (one process per GPU under torchrun).
+
+Workload "c2_p2p_pairs": ranks (2i, 2i+1) run the split-send P2P of a 1 GiB
+bf16 N(0, 0.02) shard 2i -> 2i+1 through uzip_send / uzip_recv (BASELINE
+configs[1]); value = raw bytes all pairs moved per second, timed on the device
+(CUDA events on each rank's stream, barrier + synchronize on both sides, max
+over ranks).  Alongside: the same transfer through NCCL send/recv on the same
+buffers, and the two-shot compressed allreduce of a 256 MiB bf16 activation
+tensor (configs[3]) against NCCL all_reduce.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+import torch
+import torch.distributed as dist
+
+GB = 1e9
+
+
+def _timed(fn, stream, steps, warmup, group=None):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier(group)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+    dist.barrier(group)
+    return float(ms.item()) / steps
+
+
+def run(args):
+    import bench
+    import paper_2604_17172_b200 as uz
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uz.build() if rank == 0 else None
+    dist.barrier()
+    comm = uz.Comm.from_group(None, local)
+    stream = torch.cuda.Stream()
+    n = args.bytes // 2
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1001 + rank)
+    x = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    pairs = world // 2
+    role = "send" if rank % 2 == 0 and rank + 1 < world else ("recv" if rank % 2 == 1 else "idle")
+    peer = rank + 1 if role == "send" else rank - 1
+
+    def uz_step():
+        with torch.cuda.stream(stream):
+            if role == "send":
+                comm.send(x, peer, stream)
+            elif role == "recv":
+                comm.recv(y, peer, stream)
+
+    def nccl_step():
+        with torch.cuda.stream(stream):
+            if role == "send":
+                dist.send(x, peer)
+            elif role == "recv":
+                dist.recv(y, peer)
+
+    with bench.ClockSampler(local) as clk:
+        ms = _timed(uz_step, stream, args.steps, args.warmup)
+    assert comm.async_error() == 0
+    st = comm.stats() if role == "send" else None
+    # correctness spot check: receiver sees the sender's bytes
+    ref = torch.empty_like(x)
+    if role == "send":
+        dist.send(x, peer)
+    elif role == "recv":
+        dist.recv(ref, peer)
+        assert torch.equal(ref.view(torch.int16), y.view(torch.int16)), "P2P mismatch"
+    ms_nccl = _timed(nccl_step, stream, args.steps, args.warmup)
+
+    # allreduce 256 MiB activations (two-shot compressed) vs NCCL
+    T = (256 << 20) // (2 * 4096)
+    ga = torch.Generator(device="cuda")
+    ga.manual_seed(3000 + rank)
+    scale = torch.exp(torch.randn(4096, device="cuda", generator=ga) * 0.5)
+    a = (torch.randn(T, 4096, device="cuda", generator=ga) * scale).to(torch.bfloat16)
+    ar_out = torch.empty_like(a)
+    nc_buf = a.clone()
+
+    def ar_step():
+        with torch.cuda.stream(stream):
+            comm.all_reduce(ar_out, a, stream)
+
+    def ar_nccl():
+        with torch.cuda.stream(stream):
+            dist.all_reduce(nc_buf)
+
+    ms_ar = _timed(ar_step, stream, args.steps, args.warmup)
+    ar_stats = comm.stats()
+    ms_ar_nccl = _timed(ar_nccl, stream, args.steps, args.warmup)
+    assert comm.async_error() == 0
+
+    sts = [None] * world
+    dist.all_gather_object(sts, st)
+    if rank == 0:
+        raw = pairs * 2 * n
+        ratio = next((s["wire_bytes"] / s["raw_bytes"] for s in sts if s), None)
+        wire_gbs = (ratio or 1.0) * 2 * n / (ms / 1e3) / GB
+        line = {
+            "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": bench.config_for(args), "compression_ratio": round(ratio, 5) if ratio else None,
+            "nccl_send_recv": {"value": round(raw / (ms_nccl / 1e3) / GB, 3), "unit": "GB/s",
+                               "ms_per_step": round(ms_nccl, 4)},
+            "allreduce_256MiB": {"uzip_algbw_GBps": round(2 * a.numel() / (ms_ar / 1e3) / GB, 2),
+                                 "nccl_algbw_GBps": round(2 * a.numel() / (ms_ar_nccl / 1e3) / GB, 2),
+                                 "ms": round(ms_ar, 4), "ms_nccl": round(ms_ar_nccl, 4),
+                                 "wire_ratio": round(ar_stats["wire_bytes"] / max(1, ar_stats["raw_bytes"]), 5)},
+            "roofline": {"bound": "nvlink", "kernel": "k_fused (sender: encode + P2P stores)",
+                         "achieved": round(wire_gbs, 1), "peak": 770.0, "unit": "GB/s",
+                         "peak_source": "B200_PROFILING.md measured peer copy per direction",
+                         "frac": round(wire_gbs / 770.0, 4), "traffic": None},
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * 2 * 2 * max(1, (2 * n) // (256 << 20)),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()

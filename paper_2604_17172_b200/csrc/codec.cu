@@ -8,6 +8,7 @@
 // The encoder (uzip_compress) is the E item of k_fused (fused.cu).
 #include <cstdio>
 
+#include "codec_dev.cuh"
 #include "uzip_device.cuh"
 #include "uzip_internal.h"
 
@@ -23,60 +24,22 @@ struct DecShared {
 
 __device__ __forceinline__ void set_err(CodecWs &ws, uint32_t code) { atomicCAS(ws.err, 0u, code); }
 
-// Directory entry -> payload bytes of the block; flags entries no encoder emits.
-__device__ __forceinline__ uint32_t dec_block_size(uint32_t d, uint32_t B, bool &bad) {
-  if (d == kRawBlock) return B;
-  if (d >= B / 2) {
-    bad = true;
-    return B;
-  }
-  const uint32_t sz = (uint32_t)round16(128 + 2ull * d);
-  if (sz >= B) bad = true;
-  return sz;
-}
-
 // a8: one warp decodes block b (payload at `off` within the payload section)
 // and joins it with the residual plane into `out`.
-template <int DT>
-__device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g, unsigned long long payload,
-                             uint32_t d, uint64_t b, unsigned long long off, const uint32_t *dtab, uint8_t *pay,
-                             uint8_t *symb, uint8_t *__restrict__ out, CodecWs &ws) {
+template <int DT, int B>
+__device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom &g, uint32_t d, uint64_t b,
+                               unsigned long long off, uint32_t size, const uint32_t *dtab, uint8_t *pay,
+                               uint8_t *symb, uint8_t *__restrict__ out, CodecWs &ws) {
   const int lane = threadIdx.x & 31;
-  const uint32_t B = g.B;
-  bool bad = false;
-  const uint32_t size = dec_block_size(d, B, bad);
-  if (bad || off + size > payload) {
-    if (lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
-    return;
-  }
-  const bool raw = d == kRawBlock;
-  const uint4 *srcv = reinterpret_cast<const uint4 *>(in + g.off_pay + off);
+  ResidualRegs<DT, B> R;
+  R.load(in, g, b);
+  const uint8_t *src = in + g.off_pay + off;
   uint4 *dstv = reinterpret_cast<uint4 *>(pay);
-  for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
+  for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = ld_cg_v4(src + 16 * i);
   __syncwarp();
   const uint8_t *syms = pay;
-  if (!raw) {
-    const uint32_t *pay32 = reinterpret_cast<const uint32_t *>(pay);
-    const uint16_t *pay16 = reinterpret_cast<const uint16_t *>(pay);
-    const uint32_t lt = lanemask_lt();
-    const uint32_t R = B / 32;
-    uint32_t x = pay32[lane];
-    int32_t p = (int32_t)d;
-    for (uint32_t j = 0; j < R; ++j) {
-      const uint32_t e = dtab[x & (kM - 1)];
-      symb[j * 32 + lane] = (uint8_t)e;
-      x = (e >> 20) * (x >> kProbBits) + ((e >> 8) & 0xFFFu);
-      const bool need = x < kL;
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
-      const int32_t k = __popc(m);
-      if (k > p) {
-        bad = true;
-        break;
-      }
-      if (need) x = (x << 16) | pay16[64 + p - k + __popc(m & lt)];
-      p -= k;
-    }
-    if (bad || p != 0 || __any_sync(0xFFFFFFFFu, x != kL)) {
+  if (d != kRawBlock) {
+    if (!rans_decode_warp<B>(pay, d, dtab, symb)) {
       if (lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
       __syncwarp();
       return;
@@ -84,30 +47,26 @@ __device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g
     syms = symb;
   }
   __syncwarp();
-  // join with the residual plane, 128-bit stores
-  if (DT == kF32) {
-    for (uint32_t e = lane * 4; e < B; e += 128) {
-      const uint32_t s4 = *reinterpret_cast<const uint32_t *>(syms + e);
-      const uint2 lo = ldg_nc_v2(in + g.off_res0 + 2 * (b * B + e));
-      const uint32_t h4 = ldg_nc_u32(in + g.off_res1 + b * B + e);
-      *reinterpret_cast<uint4 *>(out + 4 * (b * B + e)) = join4_f32(s4, lo, h4);
-    }
-  } else {
-    for (uint32_t e = lane * 8; e < B; e += 256) {
-      const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
-      const uint2 r8 = ld_cg_v2(in + g.off_res0 + b * B + e);
-      uint4 o;
-      if (DT == kBF16) {
-        join4_bf16(s8.x, r8.x, o.x, o.y);
-        join4_bf16(s8.y, r8.y, o.z, o.w);
-      } else {
-        join4_f16(s8.x, r8.x, o.x, o.y);
-        join4_f16(s8.y, r8.y, o.z, o.w);
-      }
-      *reinterpret_cast<uint4 *>(out + 2 * (b * B + e)) = o;
-    }
-  }
+  join_block_regs<DT, B>(syms, R, in, g, b, out + b * (uint64_t)B * g.eb);
   __syncwarp();
+}
+
+template <int DT>
+__device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g, unsigned long long payload,
+                             uint32_t d, uint64_t b, unsigned long long off, const uint32_t *dtab, uint8_t *pay,
+                             uint8_t *symb, uint8_t *__restrict__ out, CodecWs &ws) {
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  const uint32_t size = block_size(d, g.B, bad);
+  if (bad || off + size > payload) {
+    if (lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
+    return;
+  }
+  switch (g.B) {
+    case 1024: decode_block_t<DT, 1024>(in, g, d, b, off, size, dtab, pay, symb, out, ws); break;
+    case 2048: decode_block_t<DT, 2048>(in, g, d, b, off, size, dtab, pay, symb, out, ws); break;
+    default: decode_block_t<DT, 4096>(in, g, d, b, off, size, dtab, pay, symb, out, ws); break;
+  }
 }
 
 template <int DT>
@@ -207,7 +166,7 @@ __global__ void __launch_bounds__(256, 2) k_decode(const uint8_t *__restrict__ i
         unsigned long long before = 0, chunk_total = 0;
         for (uint64_t bb = c_first + tid; bb < scan_end; bb += 256) {
           bool bad = false;
-          const uint32_t sz = dec_block_size(dir[bb], B, bad);
+          const uint32_t sz = block_size(dir[bb], B, bad);
           if (bad) s_bad = 1;
           chunk_total += sz;
           if (bb < s0) before += sz;
@@ -249,7 +208,7 @@ __global__ void __launch_bounds__(256, 2) k_decode(const uint8_t *__restrict__ i
           uint32_t sz = 0;
           if (bb < seg_end) {
             bool bad = false;
-            sz = dec_block_size(dir[bb], B, bad);
+            sz = block_size(dir[bb], B, bad);
           }
           uint32_t inc2 = sz;
           for (int o = 1; o < 32; o <<= 1) {

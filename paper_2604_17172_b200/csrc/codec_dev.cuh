@@ -1,0 +1,154 @@
+// codec_dev.cuh -- device pieces of the decoder shared by k_decode (codec.cu)
+// and the D items of k_fused (fused.cu): directory sizes, decode-table build
+// (a7), 32-lane rANS decode (a8) and the join with the residual plane(s).
+#pragma once
+
+#include "uzip_device.cuh"
+
+namespace uzip {
+
+// Directory entry -> payload bytes of a block; flags entries no encoder emits.
+__device__ __forceinline__ uint32_t block_size(uint32_t d, uint32_t B, bool &bad) {
+  if (d == kRawBlock) return B;
+  if (d >= B / 2) {
+    bad = true;
+    return B;
+  }
+  const uint32_t sz = (uint32_t)round16(128 + 2ull * d);
+  if (sz >= B) bad = true;
+  return sz;
+}
+
+// Decode table of one chunk: f:12 <<20 | (slot-cdf):12 <<8 | sym:8 (a7).
+// All 256 threads; returns false (uniformly) if the table is invalid.
+__device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t f = ld_cg_u16(ft + tid);
+  uint32_t incl = f;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += tt;
+  }
+  const uint32_t anyzero = __ballot_sync(0xFFFFFFFFu, f == 0);
+  if (lane == 31) s_red[warp] = incl | (anyzero ? 0x80000000u : 0u);
+  __syncthreads();
+  uint32_t woff = 0, fsum = 0, bad = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t v = s_red[w];
+    bad |= v >> 31;
+    if (w < warp) woff += v & 0x7FFFFFFFu;
+    fsum += v & 0x7FFFFFFFu;
+  }
+  __syncthreads();
+  if (fsum != kM || bad) return false;
+  const uint32_t cdf = woff + incl - f;
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t fk = __shfl_sync(0xFFFFFFFFu, f, k);
+    const uint32_t ck = __shfl_sync(0xFFFFFFFFu, cdf, k);
+    const uint32_t sk = (uint32_t)(warp * 32 + k);
+    for (uint32_t t = lane; t < fk; t += 32) dtab[ck + t] = (fk << 20) | (t << 8) | sk;
+  }
+  return true;
+}
+
+// a8: one warp decodes the K-word block in `pay` (smem) into 8-bit symbols.
+// Returns false if the block is corrupt (word overrun, end state != L).
+template <int B>
+__device__ __forceinline__ bool rans_decode_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
+                                                 uint8_t *symb) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t *pay32 = reinterpret_cast<const uint32_t *>(pay);
+  const uint16_t *pay16 = reinterpret_cast<const uint16_t *>(pay) + 64;
+  uint32_t x = pay32[lane];
+  int32_t p = (int32_t)K;
+#pragma unroll 8
+  for (uint32_t j = 0; j < (uint32_t)(B / 32); ++j) {
+    const uint32_t e = dtab[x & (kM - 1)];
+    symb[j * 32 + lane] = (uint8_t)e;
+    x = (e >> 20) * (x >> kProbBits) + ((e >> 8) & 0xFFFu);
+    const bool need = x < kL;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
+    p -= __popc(m);
+    // the k renormalizing lanes take the last k unread words in lane order;
+    // a corrupt stream drives p negative: clamp the index, fail at the end
+    const int32_t idx = max(p + __popc(m & lt), 0);
+    const uint32_t w = pay16[idx];
+    x = need ? ((x << 16) | w) : x;
+  }
+  return !(p != 0 || __any_sync(0xFFFFFFFFu, x != kL));
+}
+
+// Join 8-bit symbols (smem) with the residual plane(s) of block b; stores B
+// elements of DT at dst (128-bit stores).
+template <int DT, int B>
+__device__ __forceinline__ void join_block(const uint8_t *syms, const uint8_t *stream, const StreamGeom &g,
+                                           uint64_t b, uint8_t *dst) {
+  const int lane = threadIdx.x & 31;
+  if (DT == kF32) {
+#pragma unroll 4
+    for (uint32_t e = lane * 4; e < (uint32_t)B; e += 128) {
+      const uint32_t s4 = *reinterpret_cast<const uint32_t *>(syms + e);
+      const uint2 lo = ld_cg_v2(stream + g.off_res0 + 2 * (b * B + e));
+      const uint32_t h4 = ld_cg_u32c(stream + g.off_res1 + b * B + e);
+      st_any16(dst + 4 * e, join4_f32(s4, lo, h4));
+    }
+  } else {
+#pragma unroll 4
+    for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
+      const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
+      const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
+      uint4 o;
+      if (DT == kBF16) {
+        join4_bf16(s8.x, r8.x, o.x, o.y);
+        join4_bf16(s8.y, r8.y, o.z, o.w);
+      } else {
+        join4_f16(s8.x, r8.x, o.x, o.y);
+        join4_f16(s8.y, r8.y, o.z, o.w);
+      }
+      st_any16(dst + 2 * e, o);
+    }
+  }
+}
+
+// Residual plane of one block held in registers (16-bit types): issued before
+// the rANS rounds so its latency hides behind them.  fp32 reads at join time.
+template <int DT, int B>
+struct ResidualRegs {
+  static constexpr int kN = (DT == kF32) ? 1 : B / 256;  // uint2 (8 residual bytes) per lane step
+  uint2 r[kN];
+  __device__ __forceinline__ void load(const uint8_t *stream, const StreamGeom &g, uint64_t b) {
+    if (DT != kF32) {
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int i = 0; i < kN; ++i) r[i] = ld_cg_v2(stream + g.off_res0 + b * B + lane * 8 + 256 * i);
+    }
+  }
+};
+
+template <int DT, int B>
+__device__ __forceinline__ void join_block_regs(const uint8_t *syms, const ResidualRegs<DT, B> &R,
+                                                const uint8_t *stream, const StreamGeom &g, uint64_t b,
+                                                uint8_t *dst) {
+  if (DT == kF32) {
+    join_block<DT, B>(syms, stream, g, b, dst);
+  } else {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < ResidualRegs<DT, B>::kN; ++i) {
+      const uint32_t e = lane * 8 + 256 * i;
+      const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
+      uint4 o;
+      if (DT == kBF16) {
+        join4_bf16(s8.x, R.r[i].x, o.x, o.y);
+        join4_bf16(s8.y, R.r[i].y, o.z, o.w);
+      } else {
+        join4_f16(s8.x, R.r[i].x, o.x, o.y);
+        join4_f16(s8.y, R.r[i].y, o.z, o.w);
+      }
+      st_any16(dst + 2 * e, o);
+    }
+  }
+}
+
+}  // namespace uzip

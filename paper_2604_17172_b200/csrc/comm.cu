@@ -93,6 +93,7 @@ uzip_config_t resolve_cfg(const uzip_config_t *in) {
 // Allocate and zero the local region and workspace of a communicator.
 uzip_status_t alloc_local(uzip_comm *c) {
   if (cudaSetDevice(c->device) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (c->cfg.staging_bytes < (2ull << 20)) return UZIP_ERR_INVALID_ARG;  // >= 2 slots of 1 MiB
   c->L.init(c->nranks, c->cfg.staging_bytes / 2);
   if (cudaMalloc(&c->region, c->L.total) != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaMemset(c->region, 0, c->L.off_stage) != cudaSuccess) return UZIP_ERR_CUDA;
@@ -101,7 +102,7 @@ uzip_status_t alloc_local(uzip_comm *c) {
   uzip_status_t st = resolve_geom(kBF16, c->L.slot_bytes / 2, &c->cfg.codec, &g);
   if (st != UZIP_OK) return st;
   c->max_chunks = g.n_chunks + 1;
-  c->ws_job_bytes = EncWs::bytes(c->max_chunks, g.n_tiles() + 1);
+  c->ws_job_bytes = EncWs::bytes(c->max_chunks, g.n_blocks + kTileBlocks);
   c->ws_bytes = 128 + (uint64_t)kMaxRanks * c->ws_job_bytes;
   if (cudaMalloc(&c->ws, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaMemset(c->ws, 0, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
@@ -145,15 +146,20 @@ uint64_t round_elems(uzip_comm *c, int dt, bool compressed, uint64_t count, Stre
   StreamGeom g;
   resolve_geom(dt, count, &c->cfg.codec, &g);
   if (g_full) *g_full = g;
-  const uint64_t unit = g.global ? (uint64_t)g.B : (uint64_t)g.CB * g.B;
-  uint64_t lo = 1, hi = std::min<uint64_t>(c->L.slot_bytes, c->cfg.pipe_chunk_bytes) / eb / unit + 1;
-  while (lo < hi) {  // largest k with bound(k*unit) <= slot and tiles/chunks within the workspace
-    const uint64_t k = (lo + hi + 1) / 2;
+  const uint64_t cap = std::min<uint64_t>(c->L.slot_bytes, c->cfg.pipe_chunk_bytes) / eb;
+  auto fits = [&](uint64_t elems) {
     StreamGeom t;
-    resolve_geom(dt, k * unit, &c->cfg.codec, &t);
-    const bool fits = t.total(t.n_blocks * (uint64_t)t.B) <= c->L.slot_bytes && t.n_tiles() + 1 <= c->L.max_tiles &&
-                      t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_tiles() + 1) <= c->ws_job_bytes;
-    if (fits) lo = k;
+    resolve_geom(dt, elems, &c->cfg.codec, &t);
+    return t.total(t.n_blocks * (uint64_t)t.B) <= c->L.slot_bytes && t.n_tiles() + 1 <= c->L.max_tiles &&
+           t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_blocks) <= c->ws_job_bytes;
+  };
+  // whole table chunks when one fits a slot, else whole tiles (a round shorter than a chunk has one chunk)
+  uint64_t unit = g.global ? (uint64_t)g.B * kTileBlocks : (uint64_t)g.CB * g.B;
+  if (!fits(unit)) unit = (uint64_t)g.B * kTileBlocks;
+  uint64_t lo = 1, hi = cap / unit + 1;
+  while (lo < hi) {  // largest k with k*unit fitting a slot and the workspace
+    const uint64_t k = (lo + hi + 1) / 2;
+    if (fits(k * unit)) lo = k;
     else hi = k - 1;
   }
   return lo * unit;
@@ -180,7 +186,7 @@ void enc_job(uzip_comm *c, Plan &p, int j, int dt, const uint8_t *in, uint64_t n
   if (compressed) {
     resolve_geom(dt, n, &c->cfg.codec, &J.g);
     J.ntiles = tiles_of(J.g);
-    EncWs::carve(ws_job(c, j), J.g.n_chunks, J.ntiles, J);
+    EncWs::carve(ws_job(c, j), J.g.n_chunks, J);
   } else {
     J.ntiles = std::max<uint64_t>(1, (J.raw_bytes + kRawTileBytes - 1) / kRawTileBytes);
   }
@@ -462,6 +468,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
   const int dt = (int)dtype;
   const uint32_t eb = elem_bytes(dt);
   const int N = c->nranks, me = c->rank;
+  if (N > 1 && (recvcount * eb) % 16 != 0) return UZIP_ERR_INVALID_ARG;  // shards stay 16-byte aligned (R21)
   const uint64_t msg = (uint64_t)N * recvcount * eb;  // R10: the user message (total input)
   const bool comp = compress_message(c, msg);
   cudaStream_t st = (cudaStream_t)stream;

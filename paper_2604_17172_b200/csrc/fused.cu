@@ -23,6 +23,7 @@
 
 #include <cstdio>
 
+#include "codec_dev.cuh"
 #include "plan.h"
 #include "uzip_internal.h"
 
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ P
   const uint32_t c = blockIdx.x;
 
   // reset the look-back words of this job for the k_fused launch that follows
-  for (uint64_t t = (uint64_t)blockIdx.x * kTabThreads + tid; t < tiles_of(g); t += (uint64_t)gridDim.x * kTabThreads)
+  for (uint64_t t = (uint64_t)blockIdx.x * kTabThreads + tid; t <= g.n_blocks; t += (uint64_t)gridDim.x * kTabThreads)
     J.tile_status[t] = 0ull;
   if (c >= g.n_chunks) return;
 
@@ -249,112 +250,6 @@ __device__ unsigned long long lookback(const Plan &P, unsigned long long *status
   return excl;
 }
 
-// Directory entry -> payload bytes of a block; flags entries no encoder emits.
-__device__ __forceinline__ uint32_t block_size(uint32_t d, uint32_t B, bool &bad) {
-  if (d == kRawBlock) return B;
-  if (d >= B / 2) {
-    bad = true;
-    return B;
-  }
-  const uint32_t sz = (uint32_t)round16(128 + 2ull * d);
-  if (sz >= B) bad = true;
-  return sz;
-}
-
-// Decode table of one chunk: f:12 <<20 | (slot-cdf):12 <<8 | sym:8 (a7).
-// All 256 threads; returns false (uniformly) if the table is invalid.
-__device__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t f = ld_cg_u16(ft + tid);
-  uint32_t incl = f;
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += tt;
-  }
-  const uint32_t anyzero = __ballot_sync(0xFFFFFFFFu, f == 0);
-  if (lane == 31) s_red[warp] = incl | (anyzero ? 0x80000000u : 0u);
-  __syncthreads();
-  uint32_t woff = 0, fsum = 0, bad = 0;
-  for (int w = 0; w < kWarps; ++w) {
-    const uint32_t v = s_red[w];
-    bad |= v >> 31;
-    if (w < warp) woff += v & 0x7FFFFFFFu;
-    fsum += v & 0x7FFFFFFFu;
-  }
-  __syncthreads();
-  if (fsum != kM || bad) return false;
-  const uint32_t cdf = woff + incl - f;
-  for (int k = 0; k < 32; ++k) {
-    const uint32_t fk = __shfl_sync(0xFFFFFFFFu, f, k);
-    const uint32_t ck = __shfl_sync(0xFFFFFFFFu, cdf, k);
-    const uint32_t sk = (uint32_t)(warp * 32 + k);
-    for (uint32_t t = lane; t < fk; t += 32) dtab[ck + t] = (fk << 20) | (t << 8) | sk;
-  }
-  return true;
-}
-
-// a8: one warp decodes the K-word block in `pay` (smem) into 8-bit symbols.
-// Returns false if the block is corrupt (word overrun, end state != L).
-template <int B>
-__device__ __forceinline__ bool rans_decode_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
-                                                 uint8_t *symb) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
-  const uint32_t *pay32 = reinterpret_cast<const uint32_t *>(pay);
-  const uint16_t *pay16 = reinterpret_cast<const uint16_t *>(pay);
-  uint32_t x = pay32[lane];
-  int32_t p = (int32_t)K;
-  bool bad = false;
-#pragma unroll 4
-  for (uint32_t j = 0; j < (uint32_t)(B / 32); ++j) {
-    const uint32_t e = dtab[x & (kM - 1)];
-    symb[j * 32 + lane] = (uint8_t)e;
-    x = (e >> 20) * (x >> kProbBits) + ((e >> 8) & 0xFFFu);
-    const bool need = x < kL;
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
-    const int32_t k = __popc(m);
-    if (k > p) {
-      bad = true;
-      break;
-    }
-    if (need) x = (x << 16) | pay16[64 + p - k + __popc(m & lt)];
-    p -= k;
-  }
-  return !(bad || p != 0 || __any_sync(0xFFFFFFFFu, x != kL));
-}
-
-// Join 8-bit symbols (smem) with the residual plane(s) of block b; stores B
-// elements of DT at dst (128-bit stores).
-template <int DT, int B>
-__device__ __forceinline__ void join_block(const uint8_t *syms, const uint8_t *stream, const StreamGeom &g,
-                                           uint64_t b, uint8_t *dst) {
-  const int lane = threadIdx.x & 31;
-  if (DT == kF32) {
-#pragma unroll 4
-    for (uint32_t e = lane * 4; e < (uint32_t)B; e += 128) {
-      const uint32_t s4 = *reinterpret_cast<const uint32_t *>(syms + e);
-      const uint2 lo = ld_cg_v2(stream + g.off_res0 + 2 * (b * B + e));
-      const uint32_t h4 = ld_cg_u32c(stream + g.off_res1 + b * B + e);
-      *reinterpret_cast<uint4 *>(dst + 4 * e) = join4_f32(s4, lo, h4);
-    }
-  } else {
-#pragma unroll 4
-    for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
-      const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
-      const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
-      uint4 o;
-      if (DT == kBF16) {
-        join4_bf16(s8.x, r8.x, o.x, o.y);
-        join4_bf16(s8.y, r8.y, o.z, o.w);
-      } else {
-        join4_f16(s8.x, r8.x, o.x, o.y);
-        join4_f16(s8.y, r8.y, o.z, o.w);
-      }
-      *reinterpret_cast<uint4 *>(dst + 2 * e) = o;
-    }
-  }
-}
-
 // ---------------------------------------------------------------- fp32 fold helpers (a9, R11)
 template <int DT>
 __device__ __forceinline__ float widen(uint32_t bits) {
@@ -405,7 +300,7 @@ template <int DT, int B>
 struct FusedCfg {
   static constexpr int kVec = (DT == kF32) ? 4 : 8;        // elements per 16-byte load
   static constexpr int kIters = B / (32 * kVec);            // loads per lane per block
-  static constexpr int kBatch = kIters < 16 ? kIters : 16;
+  static constexpr int kBatch = kIters < 8 ? kIters : 8;
   static constexpr int kRounds = B / 32;
   static constexpr int kEncTab = 4096;                      // 256 x uint4
   static constexpr int kWarpBuf = 2 * B;                    // two B-byte buffers per warp
@@ -417,32 +312,80 @@ struct FusedCfg {
 };
 
 struct FusedShared {
-  uint32_t ticket;
+  uint32_t tk[2];
   uint32_t abort;
+  uint32_t tile_cnt;
+  unsigned long long tile_off;
   uint32_t size[kWarps], k[kWarps];
   unsigned long long prefix;
   unsigned long long src_off[kMaxRanks];
   unsigned long long src_payload[kMaxRanks];
   uint32_t red[kWarps];
-  uint32_t credit_ok;
 };
 
 // ---------------------------------------------------------------- E item
+// Header (sizes before/after), zero pads and raw tail of a stream; one warp.
+template <int DT>
+__device__ void finalize_stream(const EncJob &J, unsigned long long payload) {
+  const int lane = threadIdx.x & 31;
+  const StreamGeom &g = J.g;
+  const uint64_t total = g.total(payload);
+  if (lane == 0) {
+    uint32_t h[16];
+    for (int i = 0; i < 16; ++i) h[i] = 0;
+    h[0] = 0x31425A55u;  // "UZB1"
+    h[1] = kVersion | (g.dtype << 16) | ((g.global & 1u) << 24);
+    h[2] = (uint32_t)g.n;
+    h[3] = (uint32_t)(g.n >> 32);
+    h[4] = g.B;
+    h[5] = g.CB;
+    h[6] = g.S;
+    h[7] = kProbBits | (kLanes << 8) | (kLBits << 16);
+    h[8] = (uint32_t)g.n_blocks;
+    h[9] = (uint32_t)g.n_chunks;
+    h[10] = (uint32_t)payload;
+    h[11] = (uint32_t)(payload >> 32);
+    h[12] = (uint32_t)total;
+    h[13] = (uint32_t)(total >> 32);
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      uint4 *o = reinterpret_cast<uint4 *>(J.dst[d]);
+      for (int i = 0; i < 4; ++i) o[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+    }
+    if (J.d_out_bytes) *J.d_out_bytes = total;
+    if (J.wire_acc) atomicAdd(J.wire_acc, (unsigned long long)total * J.nd);
+  }
+  const uint64_t e1 = g.off_coff + 8 * g.n_chunks, e2 = g.off_dir + 4 * g.n_blocks;
+  const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+  const uint8_t *tsrc = J.in + g.n_coded * g.eb;
+  for (uint32_t d = 0; d < J.nd; ++d) {
+    uint8_t *o = J.dst[d];
+    for (uint64_t p = e1 + lane; p < g.off_dir; p += 32) o[p] = 0;
+    for (uint64_t p = e2 + lane; p < g.off_pay; p += 32) o[p] = 0;
+    uint8_t *tdst = o + g.off_tail(payload);
+    for (uint64_t i = lane; i < tail_bytes; i += 32) tdst[i] = tsrc[i];
+  }
+}
+
+// One encode tile: every warp codes one block and finds its own offset by a
+// block-level decoupled look-back, so the warps of a CTA never wait for each
+// other; the last warp of the tile to finish releases the tile's flags.
 template <int DT, int B>
 __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &enc_key) {
+                         uint64_t &enc_key, uint32_t &credit_done) {
   using C = FusedCfg<DT, B>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    uint32_t ok = 1;
-    if (!((S.credit_ok >> jidx) & 1u)) {
+  if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
+    if (tid == 0) {
+      uint32_t ok = 1;
       for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
-      if (ok) S.credit_ok |= 1u << jidx;
+      S.abort = ok ? 0u : 1u;
     }
-    S.abort = ok ? 0u : 1u;
+    __syncthreads();
+    if (S.abort) return;
+    credit_done |= 1u << jidx;
   }
-  __syncthreads();
-  if (S.abort) return;
+  bool flags = false;
+  for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
 
   if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
     const uint64_t o0 = t * kRawTileBytes;
@@ -457,7 +400,7 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
       for (uint32_t d = 0; d < J.nd; ++d) J.dst[d][o0 + i] = v;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && flags) {
       __threadfence_system();
       for (uint32_t d = 0; d < J.nd; ++d)
         if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
@@ -474,14 +417,14 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
   const uint64_t b0 = t * kTileBlocks;
   const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
   const uint64_t key = ((uint64_t)jidx << 48) | c;
-  if (g.n_blocks && key != enc_key) {
+  if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
     tab[tid] = J.enc[c * 256 + tid];
     enc_key = key;
+    __syncthreads();
   }
-  __syncthreads();
 
   const uint64_t b = b0 + warp;
-  uint32_t K = 0, size = 0;
+  bool aborted = false;
   if (b < g.n_blocks) {
     // ---- a1: split; the residual goes straight to every destination (split-send)
     const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
@@ -519,120 +462,87 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
     }
     __syncwarp();
 
-    // ---- a4: 32 interleaved rANS lanes, rounds R-1 .. 0
+    // ---- a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body);
+    // symbols and table entries of 8 rounds are loaded ahead of their math
     const uint32_t lt = lanemask_lt();
     uint32_t x = kL;
     uint32_t wp = 0;
     constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
-#pragma unroll 4
-    for (int j = C::kRounds - 1; j >= 0; --j) {
-      const uint32_t s = sym[j * 32 + lane];
-      const uint4 e = tab[s];
-      const bool p = (x | 0x7FFFFu) >= e.y;
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
-      if (p) {
-        const uint32_t idx = wp + __popc(m & lt);
-        if (idx < kCap) blk16[64 + idx] = (uint16_t)x;
-        x >>= 16;
+    constexpr int kG = 8;
+#pragma unroll 1
+    for (int j0 = C::kRounds - 1; j0 >= 0; j0 -= kG) {
+      uint4 ent[kG];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) ent[u] = tab[sym[(j0 - u) * 32 + lane]];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const uint4 e = ent[u];
+        const bool p = (x | 0x7FFFFu) >= e.y;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+        // beyond kCap the block is stored raw anyway: clamp instead of branching
+        const uint32_t idx = min(wp + __popc(m & lt), kCap - 1);
+        if (p) blk16[64 + idx] = (uint16_t)x;
+        x = p ? (x >> 16) : x;
+        wp += __popc(m);
+        const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
+        x = x + e.z + q * e.w;
       }
-      wp += __popc(m);
-      const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
-      x = x + e.z + q * e.w;
     }
-    K = wp;
+    const uint32_t K = wp;
     const uint32_t coded = (uint32_t)round16(128 + 2ull * K);
-    if (coded >= (uint32_t)B) {
-      size = B;  // stored raw (R13)
-    } else {
-      size = coded;
+    const bool raw = coded >= (uint32_t)B;  // stored raw (R13)
+    const uint32_t size = raw ? (uint32_t)B : coded;
+    if (!raw) {
       blk32[lane] = x;
       const uint32_t pad_words = (coded - 128 - 2 * K) / 2;
       if ((uint32_t)lane < pad_words) blk16[64 + K + lane] = 0;
     }
-  }
-  if (lane == 0) {
-    S.size[warp] = size;
-    S.k[warp] = (size == (uint32_t)B) ? kRawBlock : K;
-  }
-  __syncthreads();
+    __syncwarp();
 
-  // ---- a5: tile prefix by decoupled look-back
-  if (warp == 0) {
-    unsigned long long agg = lane < kWarps ? S.size[lane] : 0u;
-    agg = warp_sum_u64(agg);
-    const unsigned long long excl = lookback(P, J.tile_status, t, agg);
-    if (lane == 0) S.prefix = excl;
-  }
-  __syncthreads();
-  if (S.prefix == ~0ull) return;  // aborted (timeout / peer error)
-
-  if (b < g.n_blocks) {
-    unsigned long long off = S.prefix;
-    for (int w = 0; w < warp; ++w) off += S.size[w];
-    const uint4 *srcv = reinterpret_cast<const uint4 *>(size == (uint32_t)B ? sym : blk);
-    for (uint32_t d = 0; d < J.nd; ++d) {
-      uint8_t *o = J.dst[d];
-      if (lane == 0) {
-        reinterpret_cast<uint32_t *>(o + g.off_dir)[b] = S.k[warp];
-        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(o + g.off_coff)[b / g.CB] = off;
-      }
-      uint4 *dstv = reinterpret_cast<uint4 *>(o + g.off_pay + off);
-      for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
-    }
-  }
-  // the chunk's first tile carries its serialized table (the receiver waits for it)
-  if (g.n_blocks && b0 % g.CB == 0 && tid < 32) {
-    const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[tid];
-    for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[tid] = v;
-  }
-  if (t == J.ntiles - 1) {  // ---- last tile: header (sizes before/after), pads, raw tail
-    unsigned long long payload = S.prefix;
-    for (int w = 0; w < kWarps; ++w) payload += S.size[w];
-    const uint64_t total = g.total(payload);
-    if (tid == 0) {
-      uint32_t h[16];
-      for (int i = 0; i < 16; ++i) h[i] = 0;
-      h[0] = 0x31425A55u;  // "UZB1"
-      h[1] = kVersion | (g.dtype << 16) | ((g.global & 1u) << 24);
-      h[2] = (uint32_t)g.n;
-      h[3] = (uint32_t)(g.n >> 32);
-      h[4] = g.B;
-      h[5] = g.CB;
-      h[6] = g.S;
-      h[7] = kProbBits | (kLanes << 8) | (kLBits << 16);
-      h[8] = (uint32_t)g.n_blocks;
-      h[9] = (uint32_t)g.n_chunks;
-      h[10] = (uint32_t)payload;
-      h[11] = (uint32_t)(payload >> 32);
-      h[12] = (uint32_t)total;
-      h[13] = (uint32_t)(total >> 32);
+    // ---- a5: block offset by decoupled look-back (this warp only)
+    const unsigned long long off = lookback(P, J.tile_status, b, size);
+    if (off == ~0ull) {
+      aborted = true;
+    } else {
+      const uint4 *srcv = reinterpret_cast<const uint4 *>(raw ? sym : blk);
       for (uint32_t d = 0; d < J.nd; ++d) {
-        uint4 *o = reinterpret_cast<uint4 *>(J.dst[d]);
-        for (int i = 0; i < 4; ++i) o[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+        uint8_t *o = J.dst[d];
+        if (lane == 0) {
+          reinterpret_cast<uint32_t *>(o + g.off_dir)[b] = raw ? kRawBlock : K;
+          if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(o + g.off_coff)[b / g.CB] = off;
+        }
+        uint4 *dstv = reinterpret_cast<uint4 *>(o + g.off_pay + off);
+        for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
       }
-      if (J.d_out_bytes) *J.d_out_bytes = total;
-      if (J.wire_acc) atomicAdd(J.wire_acc, (unsigned long long)total * J.nd);
+      if (warp == 0) {
+        if (lane == 0) S.tile_off = off;
+        // the chunk's first tile carries its serialized table (the receiver waits for it)
+        if (b0 % g.CB == 0) {
+          const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
+          for (uint32_t d = 0; d < J.nd; ++d)
+            reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
+        }
+      }
+      if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
     }
-    const uint64_t e1 = g.off_coff + 8 * g.n_chunks, e2 = g.off_dir + 4 * g.n_blocks;
-    const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
-    const uint8_t *tsrc = J.in + g.n_coded * g.eb;
-    for (uint32_t d = 0; d < J.nd; ++d) {
-      uint8_t *o = J.dst[d];
-      for (uint64_t p = e1 + tid; p < g.off_dir; p += 256) o[p] = 0;
-      for (uint64_t p = e2 + tid; p < g.off_pay; p += 256) o[p] = 0;
-      uint8_t *tdst = o + g.off_tail(payload);
-      for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
-    }
+  } else if (g.n_blocks == 0 && warp == 0) {  // no whole block: header + raw tail only
+    if (lane == 0) S.tile_off = 0;
+    finalize_stream<DT>(J, 0ull);
   }
-  __syncthreads();
-  if (tid == 0) {
-    bool any = false;
-    for (uint32_t d = 0; d < J.nd; ++d) any |= J.flag[d] != nullptr;
-    if (any) {
+  if (flags) {  // the last warp of the tile to finish releases its flags (a12)
+    __syncwarp();
+    if (lane == 0) {
       __threadfence_system();
-      const unsigned long long off16 = S.prefix >> 4;
-      for (uint32_t d = 0; d < J.nd; ++d)
-        if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+      const uint32_t inc = aborted ? 0x101u : 1u;  // low byte: warps done; above: aborted warps
+      const uint32_t now = atomicAdd(&S.tile_cnt, inc) + inc;
+      if ((now & 0xFFu) == kWarps) {
+        S.tile_cnt = 0;
+        if ((now >> 8) == 0) {  // an aborted tile is never released: its peer times out
+          const unsigned long long off16 = S.tile_off >> 4;
+          for (uint32_t d = 0; d < J.nd; ++d)
+            if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+        }
+      }
     }
   }
 }
@@ -643,7 +553,7 @@ __device__ void copy_item(const CopyJob &Cj, uint64_t t) {
   const uint64_t len = min((uint64_t)kRawTileBytes, Cj.bytes - o0);
   const uint64_t nv = len / 16;
   for (uint64_t i = threadIdx.x; i < nv; i += 256)
-    *reinterpret_cast<uint4 *>(Cj.dst + o0 + 16 * i) = ldg_nc_v4(Cj.src + o0 + 16 * i);
+    st_any16(Cj.dst + o0 + 16 * i, ldg_nc_v4(Cj.src + o0 + 16 * i));
   for (uint64_t i = nv * 16 + threadIdx.x; i < len; i += 256) Cj.dst[o0 + i] = Cj.src[o0 + i];
 }
 
@@ -729,7 +639,7 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
     const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
     const uint64_t nv = len / 16;
     for (uint64_t i = tid; i < nv; i += 256)
-      *reinterpret_cast<uint4 *>(J.out + o0 + 16 * i) = ld_cg_v4(stream + o0 + 16 * i);
+      st_any16(J.out + o0 + 16 * i, ld_cg_v4(stream + o0 + 16 * i));
     for (uint64_t i = nv * 16 + tid; i < len; i += 256) J.out[o0 + i] = stream[o0 + i];
     __syncthreads();
     dec_done(J);
@@ -754,6 +664,8 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
   tile_block(stream, g, b0, warp, S.src_off[0], K, off, tile_end, bad);
   if (b < g.n_blocks && !bad) {
     const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
+    ResidualRegs<DT, B> R;
+    R.load(stream, g, b);
     stage_payload(stream, g, off, size, pay);
     const uint8_t *syms = pay;
     if (K != kRawBlock) {
@@ -761,7 +673,7 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
       syms = symb;
     }
     __syncwarp();
-    if (!bad) join_block<DT, B>(syms, stream, g, b, J.out + b * (uint64_t)B * g.eb);
+    if (!bad) join_block_regs<DT, B>(syms, R, stream, g, b, J.out + b * (uint64_t)B * g.eb);
   }
   if (bad && (threadIdx.x & 31) == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
   if (t == J.ntiles - 1) {  // raw tail
@@ -931,22 +843,24 @@ __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
 
 // ---------------------------------------------------------------- the kernel
 template <int DT, int B, bool RED>
-__global__ void __launch_bounds__(256, RED ? 1 : 2) k_fused(const __grid_constant__ Plan P) {
+__global__ void __launch_bounds__(256, RED ? 1 : 3) k_fused(const __grid_constant__ Plan P) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ FusedShared S;
   const int tid = threadIdx.x;
   uint64_t enc_key = ~0ull, dec_key = ~0ull;
-  if (tid == 0) S.credit_ok = 0;
+  uint32_t credit_done = 0;
   const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
-  while (true) {
-    if (tid == 0) S.ticket = atomicAdd(P.ticket, 1u);
-    __syncthreads();
-    const uint64_t it = S.ticket;
-    __syncthreads();
-    if (it >= total) break;
+  if (tid == 0) {
+    S.tile_cnt = 0;
+    S.tk[0] = atomicAdd(P.ticket, 1u);
+  }
+  __syncthreads();
+  uint64_t it = S.tk[0];
+  for (int par = 0; it < total; par ^= 1) {
+    if (tid == 0) S.tk[par ^ 1] = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
     if (it < ne) {
       const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
-      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key);
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done);
     } else if (it < ne + nc) {
       copy_item(P.c, it - ne);
     } else {
@@ -957,6 +871,7 @@ __global__ void __launch_bounds__(256, RED ? 1 : 2) k_fused(const __grid_constan
       else dec_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
     }
     __syncthreads();
+    it = S.tk[par ^ 1];
   }
   if (tid == 0) {  // the last CTA out resets the ticket for the next launch
     __threadfence();

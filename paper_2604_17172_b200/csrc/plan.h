@@ -43,7 +43,7 @@ struct EncJob {
   uint32_t epoch[kMaxRanks];                // flag epoch per destination (round sequence + 1)
   uint4 *enc;                               // per-chunk encode entries (k_table)
   uint16_t *tab16;                          // per-chunk serialized tables (k_table)
-  unsigned long long *tile_status;          // look-back words (zeroed by k_table)
+  unsigned long long *tile_status;          // per-block look-back words (zeroed by k_table)
   uint64_t *d_out_bytes;                    // codec: stream size (may be null)
   unsigned long long *wire_acc;             // comm: += stream bytes x nd (may be null)
 };
@@ -86,11 +86,10 @@ struct Plan {
 // words (all written by k_table before use: no state survives a launch, so
 // the layout may change from call to call).
 struct EncWs {
-  static uint64_t bytes(uint64_t n_chunks, uint64_t n_tiles) {
-    return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * n_tiles);
+  static uint64_t bytes(uint64_t n_chunks, uint64_t n_blocks) {
+    return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * (n_blocks + 1));
   }
-  static void carve(uint8_t *p, uint64_t n_chunks, uint64_t n_tiles, EncJob &j) {
-    (void)n_tiles;
+  static void carve(uint8_t *p, uint64_t n_chunks, EncJob &j) {
     j.enc = reinterpret_cast<uint4 *>(p);
     p += round16(4096 * n_chunks);
     j.tab16 = reinterpret_cast<uint16_t *>(p);

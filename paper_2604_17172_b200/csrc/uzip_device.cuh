@@ -186,6 +186,26 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// 16-byte store to an address that is only element-aligned (allgather slices
+// of ragged counts); the alignment test is warp-uniform on every call site.
+__device__ __forceinline__ void st_any16(uint8_t *p, uint4 v) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 15) == 0) {
+    *reinterpret_cast<uint4 *>(p) = v;
+  } else if ((a & 3) == 0) {
+    uint32_t *q = reinterpret_cast<uint32_t *>(p);
+    q[0] = v.x, q[1] = v.y, q[2] = v.z, q[3] = v.w;
+  } else if ((a & 1) == 0) {
+    uint16_t *q = reinterpret_cast<uint16_t *>(p);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[2 * i] = (uint16_t)w[i], q[2 * i + 1] = (uint16_t)(w[i] >> 16);
+  } else {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+  }
+}
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
   return v;

@@ -27,6 +27,8 @@ CASES = [
      {"global_table": True, "block_symbols": 1024}),
     ("bf16_w_chunks", oracle.BF16, lambda: synth.weights(9 * 1024, 1005),
      {"block_symbols": 1024, "chunk_blocks": 4, "sample_symbols": 2000}),
+    ("bf16_w_chunks8", oracle.BF16, lambda: synth.weights(20 * 1024 + 7, 1006),
+     {"block_symbols": 1024, "chunk_blocks": 8, "sample_symbols": 3000}),
 ]
 
 

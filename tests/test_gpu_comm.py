@@ -160,7 +160,7 @@ def test_allgather(uz, nr, dtype, dist):
 def test_reduce_scatter(uz, orc, nr, dtype):
     g = Group(uz, nr, **CFG_SMALL)
     try:
-        m = (1 << 20) + 4096 * 2 + 3  # per-rank shard (ragged tail)
+        m = (1 << 20) + 4096 * 2 + 8  # per-rank shard (ragged tail, 16-byte aligned shards)
         ins = [gen("W", nr * m, 77 + r, dtype) for r in range(nr)]
         xs = [dev(b, dtype) for b in ins]
         outs = [torch.empty(m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
@@ -210,12 +210,25 @@ def test_allreduce_in_place_and_transparency(uz, orc):
         assert np.array_equal(results["off"][r], ref)
 
 
+def test_reduce_scatter_rejects_unaligned_shards(uz):
+    g = Group(uz, 2, **CFG_SMALL)
+    try:
+        x = torch.zeros(2 * 1001, dtype=torch.bfloat16, device="cuda")
+        y = torch.zeros(1001, dtype=torch.bfloat16, device="cuda")
+        with pytest.raises(uz.UzipError):
+            g.comms[0].reduce_scatter(y, x)
+        with pytest.raises(uz.UzipError):
+            g.comms[0].all_reduce(x)
+    finally:
+        g.close()
+
+
 def test_below_threshold_raw_path(uz, orc):
     """Messages under min_compress_bytes move raw, same results."""
     nr = 2
     g = Group(uz, nr, staging_bytes=4 << 20)  # default threshold 1 MiB
     try:
-        n = 1000 * 2 + 2  # < 1 MiB
+        n = 2 * 1008  # < 1 MiB, 16-byte shards
         ins = [synth.weights(n, 9 + r) for r in range(nr)]
         xs = [dev(b, BF16) for b in ins]
         outs = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
