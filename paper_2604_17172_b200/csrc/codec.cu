@@ -18,7 +18,7 @@ namespace uzip {
 struct DecShared {
   static constexpr int kTab = 4096 * 4;          // decode table
   static constexpr int kOff = 1024 * 4;          // per-segment block offsets (relative to chunk)
-  static constexpr int kWarpBuf = 2 * kMaxB;     // payload + symbols
+  static constexpr int kWarpBuf = kMaxB + 256;   // staged payload + 8-round symbol ring
   static constexpr int kBytes = kTab + kOff + kWarps * kWarpBuf;
 };
 
@@ -29,32 +29,25 @@ __device__ __forceinline__ void set_err(CodecWs &ws, uint32_t code) { atomicCAS(
 template <int DT, int B>
 __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom &g, uint32_t d, uint64_t b,
                                unsigned long long off, uint32_t size, const uint32_t *dtab, uint8_t *pay,
-                               uint8_t *symb, uint8_t *__restrict__ out, CodecWs &ws) {
+                               uint8_t *ring, uint8_t *__restrict__ out, CodecWs &ws) {
   const int lane = threadIdx.x & 31;
-  ResidualRegs<DT, B> R;
-  R.load(in, g, b);
   const uint8_t *src = in + g.off_pay + off;
   uint4 *dstv = reinterpret_cast<uint4 *>(pay);
   for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = ld_cg_v4(src + 16 * i);
   __syncwarp();
-  const uint8_t *syms = pay;
-  if (d != kRawBlock) {
-    if (!rans_decode_warp<B>(pay, d, dtab, symb)) {
-      if (lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
-      __syncwarp();
-      return;
-    }
-    syms = symb;
+  uint8_t *dst = out + b * (uint64_t)B * g.eb;
+  if (d == kRawBlock) {
+    join_block<DT, B>(pay, in, g, b, dst);
+  } else if (!decode_join_warp<DT, B>(pay, d, dtab, ring, in, g, b, dst)) {
+    if (lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
   }
-  __syncwarp();
-  join_block_regs<DT, B>(syms, R, in, g, b, out + b * (uint64_t)B * g.eb);
   __syncwarp();
 }
 
 template <int DT>
 __device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g, unsigned long long payload,
                              uint32_t d, uint64_t b, unsigned long long off, const uint32_t *dtab, uint8_t *pay,
-                             uint8_t *symb, uint8_t *__restrict__ out, CodecWs &ws) {
+                             uint8_t *ring, uint8_t *__restrict__ out, CodecWs &ws) {
   const int lane = threadIdx.x & 31;
   bool bad = false;
   const uint32_t size = block_size(d, g.B, bad);
@@ -63,14 +56,14 @@ __device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g
     return;
   }
   switch (g.B) {
-    case 1024: decode_block_t<DT, 1024>(in, g, d, b, off, size, dtab, pay, symb, out, ws); break;
-    case 2048: decode_block_t<DT, 2048>(in, g, d, b, off, size, dtab, pay, symb, out, ws); break;
-    default: decode_block_t<DT, 4096>(in, g, d, b, off, size, dtab, pay, symb, out, ws); break;
+    case 1024: decode_block_t<DT, 1024>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
+    case 2048: decode_block_t<DT, 2048>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
+    default: decode_block_t<DT, 4096>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
   }
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256, 2) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
+__global__ void __launch_bounds__(256, 3) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
                                                   uint8_t *__restrict__ out, uint64_t n, CodecWs ws,
                                                   int32_t *__restrict__ d_status) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -78,7 +71,7 @@ __global__ void __launch_bounds__(256, 2) k_decode(const uint8_t *__restrict__ i
   uint32_t *soff = reinterpret_cast<uint32_t *>(smem + DecShared::kTab);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t *pay = smem + DecShared::kTab + DecShared::kOff + warp * DecShared::kWarpBuf;
-  uint8_t *symb = pay + kMaxB;
+  uint8_t *ring = pay + kMaxB;
 
   __shared__ uint32_t s_red[kWarps];
   __shared__ uint32_t s_bad;
@@ -229,7 +222,7 @@ __global__ void __launch_bounds__(256, 2) k_decode(const uint8_t *__restrict__ i
         // ---- a8: warp per block
         for (uint64_t b = seg + warp; b < seg_end; b += kWarps) {
           const unsigned long long off = cbase + run0 + soff[b - seg];
-          decode_block<DT>(in, g, payload, dir[b], b, off, dtab, pay, symb, out, ws);
+          decode_block<DT>(in, g, payload, dir[b], b, off, dtab, pay, ring, out, ws);
         }
         __syncthreads();
         if (tid == 0) s_base = run;

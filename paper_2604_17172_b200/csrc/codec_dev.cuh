@@ -151,4 +151,87 @@ __device__ __forceinline__ void join_block_regs(const uint8_t *syms, const Resid
   }
 }
 
+// a8 + join, streamed: one warp decodes a coded block 8 rounds at a time.
+// The 8 rounds x 32 lanes of symbols land in a 256-byte ring (element order
+// within the group), each lane then joins ITS 8 consecutive elements with the
+// residual bytes it prefetched kPF groups earlier and stores 16 bytes (fp32:
+// 32).  Per warp this needs the staged payload plus 256 bytes of smem, so more
+// warps (rANS chains) fit on an SM.  Returns false on a corrupt block.
+template <int DT, int B>
+__device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
+                                                 uint8_t *ring, const uint8_t *stream, const StreamGeom &g,
+                                                 uint64_t b, uint8_t *dst) {
+  constexpr int kGroups = B / 256;
+  constexpr int kPF = 4;  // residual prefetch distance in groups (divides kGroups)
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t *pay32 = reinterpret_cast<const uint32_t *>(pay);
+  const uint16_t *pay16 = reinterpret_cast<const uint16_t *>(pay) + 64;
+  const uint8_t *res0 = stream + g.off_res0 + (DT == kF32 ? 2 : 1) * (b * B) + (DT == kF32 ? 16 : 8) * lane;
+  const uint8_t *res1 = stream + g.off_res1 + b * B + 8 * lane;  // fp32 hi8 plane
+  uint4 rlo[kPF];   // fp32: lo16 of 8 elements; 16-bit types: .x/.y = 8 residual bytes
+  uint2 rhi[kPF];   // fp32: hi8 of 8 elements
+#pragma unroll
+  for (int i = 0; i < kPF; ++i) {
+    if (DT == kF32) {
+      rlo[i] = ld_cg_v4(res0 + 512 * i);
+      rhi[i] = ld_cg_v2(res1 + 256 * i);
+    } else {
+      const uint2 v = ld_cg_v2(res0 + 256 * i);
+      rlo[i] = make_uint4(v.x, v.y, 0, 0);
+    }
+  }
+  uint32_t x = pay32[lane];
+  int32_t p = (int32_t)K;
+#pragma unroll 1
+  for (int g0 = 0; g0 < kGroups; g0 += kPF) {
+#pragma unroll
+    for (int q = 0; q < kPF; ++q) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = dtab[x & (kM - 1)];
+        ring[u * 32 + lane] = (uint8_t)e;
+        x = (e >> 20) * (x >> kProbBits) + ((e >> 8) & 0xFFFu);
+        const bool need = x < kL;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
+        p -= __popc(m);
+        // the k renormalizing lanes take the last k unread words in lane order;
+        // a corrupt stream drives p negative: clamp the index, fail at the end
+        const int32_t idx = max(p + __popc(m & lt), 0);
+        const uint32_t w = pay16[idx];
+        x = need ? ((x << 16) | w) : x;
+      }
+      __syncwarp();
+      const uint2 s8 = *reinterpret_cast<const uint2 *>(ring + 8 * lane);
+      const int gi = g0 + q;
+      uint8_t *o = dst + (DT == kF32 ? 4 : 2) * (256 * gi + 8 * lane);
+      if (DT == kF32) {
+        st_any16(o, join4_f32(s8.x, make_uint2(rlo[q].x, rlo[q].y), rhi[q].x));
+        st_any16(o + 16, join4_f32(s8.y, make_uint2(rlo[q].z, rlo[q].w), rhi[q].y));
+      } else {
+        uint4 v;
+        if (DT == kBF16) {
+          join4_bf16(s8.x, rlo[q].x, v.x, v.y);
+          join4_bf16(s8.y, rlo[q].y, v.z, v.w);
+        } else {
+          join4_f16(s8.x, rlo[q].x, v.x, v.y);
+          join4_f16(s8.y, rlo[q].y, v.z, v.w);
+        }
+        st_any16(o, v);
+      }
+      if (gi + kPF < kGroups) {
+        if (DT == kF32) {
+          rlo[q] = ld_cg_v4(res0 + 512 * (gi + kPF));
+          rhi[q] = ld_cg_v2(res1 + 256 * (gi + kPF));
+        } else {
+          const uint2 v = ld_cg_v2(res0 + 256 * (gi + kPF));
+          rlo[q] = make_uint4(v.x, v.y, 0, 0);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  return !(p != 0 || __any_sync(0xFFFFFFFFu, x != kL));
+}
+
 }  // namespace uzip

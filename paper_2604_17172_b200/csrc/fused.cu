@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ P
   const uint32_t c = blockIdx.x;
 
   // reset the look-back words of this job for the k_fused launch that follows
-  for (uint64_t t = (uint64_t)blockIdx.x * kTabThreads + tid; t <= g.n_blocks; t += (uint64_t)gridDim.x * kTabThreads)
+  for (uint64_t t = (uint64_t)blockIdx.x * kTabThreads + tid; t < tiles_of(g); t += (uint64_t)gridDim.x * kTabThreads)
     J.tile_status[t] = 0ull;
   if (c >= g.n_chunks) return;
 
@@ -366,13 +366,16 @@ __device__ void finalize_stream(const EncJob &J, unsigned long long payload) {
   }
 }
 
-// One encode tile: every warp codes one block and finds its own offset by a
-// block-level decoupled look-back, so the warps of a CTA never wait for each
-// other; the last warp of the tile to finish releases the tile's flags.
+// One encode tile: every warp codes one block; one warp finds the tile's
+// offset by decoupled look-back over tiles; the last warp of the tile to
+// finish its stores releases the tile's flags.
 template <int DT, int B>
 __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &enc_key, uint32_t &credit_done) {
+                         uint64_t &enc_key, uint32_t &credit_done, uint64_t it, uint64_t next_it,
+                         uint64_t &presplit) {
   using C = FusedCfg<DT, B>;
+  const bool have_pre = presplit == it;  // this warp's block was split during the previous tile
+  presplit = ~0ull;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
     if (tid == 0) {
@@ -424,12 +427,13 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
   }
 
   const uint64_t b = b0 + warp;
-  bool aborted = false;
+  uint32_t size = 0, kdir = 0;
+  bool raw = false;
   if (b < g.n_blocks) {
     // ---- a1: split; the residual goes straight to every destination (split-send)
     const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
 #pragma unroll
-    for (int h = 0; h < C::kIters; h += C::kBatch) {
+    for (int h = 0; h < (have_pre ? 0 : C::kIters); h += C::kBatch) {
       uint4 v[C::kBatch];
 #pragma unroll
       for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
@@ -463,85 +467,159 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
     __syncwarp();
 
     // ---- a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body);
-    // symbols and table entries of 8 rounds are loaded ahead of their math
+    // symbols and table entries of 8 rounds are loaded ahead of their math.
+    // Software pipeline (2-byte types): while this block is coded, the NEXT
+    // tile's block (prefetched ticket) is loaded kPF groups ahead and split
+    // into the symbol rows this block has already consumed, its residual
+    // leaving for its destinations at once -- no exposed load latency.
+    const EncJob *NJ = nullptr;
+    uint64_t nblk = 0;
+    if (DT != kF32 && next_it < P.n_e_items) {
+      const int nj = (int)(next_it % (uint64_t)P.ne);
+      const EncJob &Jn = P.e[nj];
+      const uint64_t nb = (next_it / (uint64_t)P.ne) * kTileBlocks + warp;
+      if (!Jn.raw && ((credit_done >> nj) & 1u) && nb < Jn.g.n_blocks) {
+        NJ = &Jn;
+        nblk = nb;
+        presplit = next_it;
+      }
+    }
+    constexpr int kGroups = C::kRounds / 8;
+    constexpr int kPF = 4;  // prefetch distance in 8-round groups (divides kGroups)
+    const uint8_t *nsrc = NJ ? NJ->in + nblk * (uint64_t)B * elem_bytes(DT) + 16 * lane : nullptr;
+    uint4 pre[kPF];
+    if (NJ) {
+#pragma unroll
+      for (int q = 0; q < kPF; ++q) pre[q] = ldg_nc_v4(nsrc + 512 * (kGroups - 1 - q));
+    }
     const uint32_t lt = lanemask_lt();
     uint32_t x = kL;
     uint32_t wp = 0;
     constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
     constexpr int kG = 8;
 #pragma unroll 1
-    for (int j0 = C::kRounds - 1; j0 >= 0; j0 -= kG) {
-      uint4 ent[kG];
+    for (int k0 = kGroups - 1; k0 >= 0; k0 -= kPF) {
 #pragma unroll
-      for (int u = 0; u < kG; ++u) ent[u] = tab[sym[(j0 - u) * 32 + lane]];
+      for (int q = 0; q < kPF; ++q) {
+        const int k = k0 - q;  // group k = rounds 8k .. 8k+7
+        const int j0 = 8 * k + 7;
+        uint4 ent[kG];
 #pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        const uint4 e = ent[u];
-        const bool p = (x | 0x7FFFFu) >= e.y;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
-        // beyond kCap the block is stored raw anyway: clamp instead of branching
-        const uint32_t idx = min(wp + __popc(m & lt), kCap - 1);
-        if (p) blk16[64 + idx] = (uint16_t)x;
-        x = p ? (x >> 16) : x;
-        wp += __popc(m);
-        const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
-        x = x + e.z + q * e.w;
+        for (int u = 0; u < kG; ++u) ent[u] = tab[sym[(j0 - u) * 32 + lane]];
+#pragma unroll
+        for (int u = 0; u < kG; ++u) {
+          const uint4 e = ent[u];
+          const bool p = (x | 0x7FFFFu) >= e.y;
+          const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+          // beyond kCap the block is stored raw anyway: clamp instead of branching
+          const uint32_t idx = min(wp + __popc(m & lt), kCap - 1);
+          if (p) blk16[64 + idx] = (uint16_t)x;
+          x = p ? (x >> 16) : x;
+          wp += __popc(m);
+          const uint32_t qq = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
+          x = x + e.z + qq * e.w;
+        }
+        if (NJ) {  // split the next block's group k into the rows just consumed
+          __syncwarp();
+          const uint4 v = pre[q];
+          if (k - kPF >= 0) pre[q] = ldg_nc_v4(nsrc + 512 * (k - kPF));
+          uint32_t s0, s1, r0, r1;
+          if (DT == kBF16) {
+            split4_bf16(v.x, v.y, s0, r0);
+            split4_bf16(v.z, v.w, s1, r1);
+          } else {
+            split4_f16(v.x, v.y, s0, r0);
+            split4_f16(v.z, v.w, s1, r1);
+          }
+          const uint32_t e = 256 * k + 8 * lane;
+          *reinterpret_cast<uint2 *>(sym + e) = make_uint2(s0, s1);
+          const StreamGeom &gn = NJ->g;
+          for (uint32_t d = 0; d < NJ->nd; ++d)
+            *reinterpret_cast<uint2 *>(NJ->dst[d] + gn.off_res0 + nblk * B + e) = make_uint2(r0, r1);
+        }
       }
     }
     const uint32_t K = wp;
     const uint32_t coded = (uint32_t)round16(128 + 2ull * K);
-    const bool raw = coded >= (uint32_t)B;  // stored raw (R13)
-    const uint32_t size = raw ? (uint32_t)B : coded;
+    raw = coded >= (uint32_t)B;  // stored raw (R13)
+    size = raw ? (uint32_t)B : coded;
+    kdir = raw ? kRawBlock : K;
     if (!raw) {
       blk32[lane] = x;
       const uint32_t pad_words = (coded - 128 - 2 * K) / 2;
       if ((uint32_t)lane < pad_words) blk16[64 + K + lane] = 0;
+    } else {
+      // stored raw: the payload is the block's symbols; `sym` may already hold
+      // the next block's, so split them again from the input into blk (rare path)
+      __syncwarp();
+      for (uint32_t v = lane; v < (uint32_t)(C::kIters * 32); v += 32) {
+        const uint4 w = ldg_nc_v4(src + 16 * (size_t)v);
+        const uint32_t e = v * C::kVec;
+        if (DT == kF32) {
+          uint32_t s4, h4;
+          uint2 lo;
+          split4_f32(w, s4, lo, h4);
+          *reinterpret_cast<uint32_t *>(blk + e) = s4;
+        } else {
+          uint32_t s0, s1, r0, r1;
+          if (DT == kBF16) {
+            split4_bf16(w.x, w.y, s0, r0);
+            split4_bf16(w.z, w.w, s1, r1);
+          } else {
+            split4_f16(w.x, w.y, s0, r0);
+            split4_f16(w.z, w.w, s1, r1);
+          }
+          *reinterpret_cast<uint2 *>(blk + e) = make_uint2(s0, s1);
+        }
+      }
     }
     __syncwarp();
+  }
+  if (lane == 0) S.size[warp] = size;
+  __syncthreads();
 
-    // ---- a5: block offset by decoupled look-back (this warp only)
-    const unsigned long long off = lookback(P, J.tile_status, b, size);
-    if (off == ~0ull) {
-      aborted = true;
-    } else {
-      const uint4 *srcv = reinterpret_cast<const uint4 *>(raw ? sym : blk);
-      for (uint32_t d = 0; d < J.nd; ++d) {
-        uint8_t *o = J.dst[d];
-        if (lane == 0) {
-          reinterpret_cast<uint32_t *>(o + g.off_dir)[b] = raw ? kRawBlock : K;
-          if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(o + g.off_coff)[b / g.CB] = off;
-        }
-        uint4 *dstv = reinterpret_cast<uint4 *>(o + g.off_pay + off);
-        for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
+  // ---- a5: tile prefix by decoupled look-back (one warp per tile)
+  if (warp == 0) {
+    unsigned long long agg = lane < kWarps ? S.size[lane] : 0u;
+    agg = warp_sum_u64(agg);
+    const unsigned long long excl = lookback(P, J.tile_status, t, agg);
+    if (lane == 0) S.tile_off = excl;
+  }
+  __syncthreads();
+  const unsigned long long tile_off = S.tile_off;
+  if (tile_off == ~0ull) return;  // aborted (timeout / peer error)
+
+  if (b < g.n_blocks) {
+    unsigned long long off = tile_off;
+    for (int w = 0; w < warp; ++w) off += S.size[w];
+    const uint4 *srcv = reinterpret_cast<const uint4 *>(blk);
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      uint8_t *o = J.dst[d];
+      if (lane == 0) {
+        reinterpret_cast<uint32_t *>(o + g.off_dir)[b] = kdir;
+        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(o + g.off_coff)[b / g.CB] = off;
       }
-      if (warp == 0) {
-        if (lane == 0) S.tile_off = off;
-        // the chunk's first tile carries its serialized table (the receiver waits for it)
-        if (b0 % g.CB == 0) {
-          const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
-          for (uint32_t d = 0; d < J.nd; ++d)
-            reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
-        }
-      }
-      if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
+      uint4 *dstv = reinterpret_cast<uint4 *>(o + g.off_pay + off);
+      for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
     }
+    if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
   } else if (g.n_blocks == 0 && warp == 0) {  // no whole block: header + raw tail only
-    if (lane == 0) S.tile_off = 0;
     finalize_stream<DT>(J, 0ull);
   }
-  if (flags) {  // the last warp of the tile to finish releases its flags (a12)
+  // the chunk's first tile carries its serialized table (the receiver waits for it)
+  if (g.n_blocks && b0 % g.CB == 0 && warp == kWarps - 1) {
+    const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
+    for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
+  }
+  if (flags) {  // the last warp of the tile to finish its stores releases the tile's flags (a12)
     __syncwarp();
     if (lane == 0) {
       __threadfence_system();
-      const uint32_t inc = aborted ? 0x101u : 1u;  // low byte: warps done; above: aborted warps
-      const uint32_t now = atomicAdd(&S.tile_cnt, inc) + inc;
-      if ((now & 0xFFu) == kWarps) {
+      if (atomicAdd(&S.tile_cnt, 1u) == kWarps - 1) {
         S.tile_cnt = 0;
-        if ((now >> 8) == 0) {  // an aborted tile is never released: its peer times out
-          const unsigned long long off16 = S.tile_off >> 4;
-          for (uint32_t d = 0; d < J.nd; ++d)
-            if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
-        }
+        const unsigned long long off16 = tile_off >> 4;
+        for (uint32_t d = 0; d < J.nd; ++d)
+          if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
       }
     }
   }
@@ -664,16 +742,11 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
   tile_block(stream, g, b0, warp, S.src_off[0], K, off, tile_end, bad);
   if (b < g.n_blocks && !bad) {
     const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
-    ResidualRegs<DT, B> R;
-    R.load(stream, g, b);
     stage_payload(stream, g, off, size, pay);
-    const uint8_t *syms = pay;
-    if (K != kRawBlock) {
-      if (!rans_decode_warp<B>(pay, K, dtab, symb)) bad = true;
-      syms = symb;
-    }
+    uint8_t *dst = J.out + b * (uint64_t)B * g.eb;
+    if (K == kRawBlock) join_block<DT, B>(pay, stream, g, b, dst);
+    else if (!decode_join_warp<DT, B>(pay, K, dtab, symb, stream, g, b, dst)) bad = true;
     __syncwarp();
-    if (!bad) join_block_regs<DT, B>(syms, R, stream, g, b, J.out + b * (uint64_t)B * g.eb);
   }
   if (bad && (threadIdx.x & 31) == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
   if (t == J.ntiles - 1) {  // raw tail
@@ -847,7 +920,7 @@ __global__ void __launch_bounds__(256, RED ? 1 : 3) k_fused(const __grid_constan
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ FusedShared S;
   const int tid = threadIdx.x;
-  uint64_t enc_key = ~0ull, dec_key = ~0ull;
+  uint64_t enc_key = ~0ull, dec_key = ~0ull, presplit = ~0ull;
   uint32_t credit_done = 0;
   const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
   if (tid == 0) {
@@ -860,7 +933,9 @@ __global__ void __launch_bounds__(256, RED ? 1 : 3) k_fused(const __grid_constan
     if (tid == 0) S.tk[par ^ 1] = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
     if (it < ne) {
       const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
-      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done);
+      __syncthreads();  // the next ticket is visible: the encoder pre-splits that tile
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, it, S.tk[par ^ 1],
+                      presplit);
     } else if (it < ne + nc) {
       copy_item(P.c, it - ne);
     } else {
