@@ -157,10 +157,25 @@ __device__ __forceinline__ void join_block_regs(const uint8_t *syms, const Resid
 // residual bytes it prefetched kPF groups earlier and stores 16 bytes (fp32:
 // 32).  Per warp this needs the staged payload plus 256 bytes of smem, so more
 // warps (rANS chains) fit on an SM.  Returns false on a corrupt block.
-template <int DT, int B>
-__device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
-                                                 uint8_t *ring, const uint8_t *stream, const StreamGeom &g,
-                                                 uint64_t b, uint8_t *dst) {
+// Epilogue of the streamed decoder: receives the 8 joined elements of a lane
+// (element offset e0 within the block; fp32 uses both vectors).
+struct StoreEpi {
+  uint8_t *dst;
+  template <int DT>
+  __device__ __forceinline__ void apply(uint32_t e0, uint4 a, uint4 b) const {
+    if (DT == kF32) {
+      st_any16(dst + 4 * e0, a);
+      st_any16(dst + 4 * e0 + 16, b);
+    } else {
+      st_any16(dst + 2 * e0, a);
+    }
+  }
+};
+
+template <int DT, int B, class Epi>
+__device__ __forceinline__ bool decode_join_warp_epi(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
+                                                     uint8_t *ring, const uint8_t *stream, const StreamGeom &g,
+                                                     uint64_t b, const Epi &epi) {
   constexpr int kGroups = B / 256;
   constexpr int kPF = 4;  // residual prefetch distance in groups (divides kGroups)
   const int lane = threadIdx.x & 31;
@@ -204,10 +219,10 @@ __device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K,
       __syncwarp();
       const uint2 s8 = *reinterpret_cast<const uint2 *>(ring + 8 * lane);
       const int gi = g0 + q;
-      uint8_t *o = dst + (DT == kF32 ? 4 : 2) * (256 * gi + 8 * lane);
+      const uint32_t e0 = 256 * gi + 8 * lane;
       if (DT == kF32) {
-        st_any16(o, join4_f32(s8.x, make_uint2(rlo[q].x, rlo[q].y), rhi[q].x));
-        st_any16(o + 16, join4_f32(s8.y, make_uint2(rlo[q].z, rlo[q].w), rhi[q].y));
+        epi.template apply<DT>(e0, join4_f32(s8.x, make_uint2(rlo[q].x, rlo[q].y), rhi[q].x),
+                               join4_f32(s8.y, make_uint2(rlo[q].z, rlo[q].w), rhi[q].y));
       } else {
         uint4 v;
         if (DT == kBF16) {
@@ -217,7 +232,7 @@ __device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K,
           join4_f16(s8.x, rlo[q].x, v.x, v.y);
           join4_f16(s8.y, rlo[q].y, v.z, v.w);
         }
-        st_any16(o, v);
+        epi.template apply<DT>(e0, v, v);
       }
       if (gi + kPF < kGroups) {
         if (DT == kF32) {
@@ -232,6 +247,14 @@ __device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K,
     }
   }
   return !(p != 0 || __any_sync(0xFFFFFFFFu, x != kL));
+}
+
+template <int DT, int B>
+__device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
+                                                 uint8_t *ring, const uint8_t *stream, const StreamGeom &g,
+                                                 uint64_t b, uint8_t *dst) {
+  StoreEpi epi{dst};
+  return decode_join_warp_epi<DT, B>(pay, K, dtab, ring, stream, g, b, epi);
 }
 
 }  // namespace uzip

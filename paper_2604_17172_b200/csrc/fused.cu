@@ -303,7 +303,7 @@ struct FusedCfg {
   static constexpr int kBatch = kIters < 8 ? kIters : 8;
   static constexpr int kRounds = B / 32;
   static constexpr int kEncTab = 4096;                      // 256 x uint4
-  static constexpr int kWarpBuf = 2 * B;                    // two B-byte buffers per warp
+  static constexpr int kWarpBuf = B + 256;                  // per warp: symbols/words (E) or payload + ring (D)
   static constexpr int kDecTab = 4096 * 4;
   static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce)
   static constexpr int smem(bool dec, bool red) {
@@ -366,16 +366,110 @@ __device__ void finalize_stream(const EncJob &J, unsigned long long payload) {
   }
 }
 
+// a1: split block b.  REV: symbol rows in coding order (row of round j at
+// (R-1-j)*32, lanes in order within a row) for the encoder; otherwise element
+// order (the stored-raw payload).  RES: also store the residual plane(s) to
+// every destination (split-send: they leave before the exponents are coded).
+template <int DT, int B, bool RES, bool REV>
+__device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
+                                            uint8_t *buf) {
+  using C = FusedCfg<DT, B>;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 0; h < C::kIters; h += C::kBatch) {
+    uint4 v[C::kBatch];
+#pragma unroll
+    for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
+#pragma unroll
+    for (int i = 0; i < C::kBatch; ++i) {
+      const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;            // element within block
+      const uint32_t pos = REV ? (uint32_t)(B - 32) - (e & ~31u) + (e & 31u) : e;  // byte in buf
+      if (DT == kF32) {
+        uint32_t s4, h4;
+        uint2 lo;
+        split4_f32(v[i], s4, lo, h4);
+        *reinterpret_cast<uint32_t *>(buf + pos) = s4;
+        if (RES)
+          for (uint32_t d = 0; d < J.nd; ++d) {
+            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
+            *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
+          }
+      } else {
+        uint32_t s0, s1, r0, r1;
+        if (DT == kBF16) {
+          split4_bf16(v[i].x, v[i].y, s0, r0);
+          split4_bf16(v[i].z, v[i].w, s1, r1);
+        } else {
+          split4_f16(v[i].x, v[i].y, s0, r0);
+          split4_f16(v[i].z, v[i].w, s1, r1);
+        }
+        *reinterpret_cast<uint2 *>(buf + pos) = make_uint2(s0, s1);
+        if (RES)
+          for (uint32_t d = 0; d < J.nd; ++d)
+            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(r0, r1);
+      }
+    }
+  }
+}
+
+// a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body); the
+// symbols and table entries of 8 rounds are loaded ahead of their math.
+// Words are compacted (ballot + popc) into emission order.  GLOBAL = false:
+// words go to buf, behind the rows already read (limit 16 words per consumed
+// row); a word that would overtake them sets `ovf` and is dropped.  GLOBAL =
+// true (rare path): words go straight to every destination at payload offset
+// `off` + 128.
+template <int DT, int B, bool GLOBAL>
+__device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &g, unsigned long long off,
+                                             uint8_t *buf, const uint4 *tab, uint32_t &x_out, uint32_t &K,
+                                             bool &ovf) {
+  using C = FusedCfg<DT, B>;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
+  uint32_t x = kL, wp = 0;
+  bool over = false;
+  constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
+  constexpr int kG = 8;
+#pragma unroll 1
+  for (int G = 0; G < C::kRounds / kG; ++G) {
+    uint4 ent[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) ent[u] = tab[buf[(kG * G + u) * 32 + lane]];
+    __syncwarp();  // every lane read these rows before words may land in them
+    const uint32_t lim = GLOBAL ? kCap : min(kCap, (uint32_t)(16 * kG) * (G + 1));
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const uint4 e = ent[u];
+      const bool p = (x | 0x7FFFFu) >= e.y;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+      const uint32_t idx = min(wp + __popc(m & lt), lim - 1);  // clamped words are never used
+      if (GLOBAL) {
+        if (p && idx + 1 < kCap)
+          for (uint32_t d = 0; d < J.nd; ++d)
+            *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + 2 * idx) = (uint16_t)x;
+      } else if (p) {
+        buf16[idx] = (uint16_t)x;
+      }
+      x = p ? (x >> 16) : x;
+      wp += __popc(m);
+      const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
+      x = x + e.z + q * e.w;
+    }
+    over |= wp > lim;
+  }
+  x_out = x;
+  K = wp;
+  ovf = over;
+}
+
 // One encode tile: every warp codes one block; one warp finds the tile's
 // offset by decoupled look-back over tiles; the last warp of the tile to
 // finish its stores releases the tile's flags.
 template <int DT, int B>
 __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &enc_key, uint32_t &credit_done, uint64_t it, uint64_t next_it,
-                         uint64_t &presplit) {
+                         uint64_t &enc_key, uint32_t &credit_done) {
   using C = FusedCfg<DT, B>;
-  const bool have_pre = presplit == it;  // this warp's block was split during the previous tile
-  presplit = ~0ull;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
     if (tid == 0) {
@@ -413,10 +507,10 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
 
   const StreamGeom &g = J.g;
   uint4 *tab = reinterpret_cast<uint4 *>(smem);
-  uint8_t *sym = smem + C::kEncTab + warp * C::kWarpBuf;
-  uint8_t *blk = sym + B;
-  uint16_t *blk16 = reinterpret_cast<uint16_t *>(blk);
-  uint32_t *blk32 = reinterpret_cast<uint32_t *>(blk);
+  // One B-byte buffer per warp: symbol rows stored in coding order (round R-1
+  // first); the coded words grow from byte 0 into the rows already consumed.
+  uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
   const uint64_t b0 = t * kTileBlocks;
   const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
   const uint64_t key = ((uint64_t)jidx << 48) | c;
@@ -427,151 +521,23 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
   }
 
   const uint64_t b = b0 + warp;
-  uint32_t size = 0, kdir = 0;
-  bool raw = false;
+  const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
+  uint32_t size = 0, kdir = 0, K = 0, x = kL;
+  bool raw = false, ovf = false;
   if (b < g.n_blocks) {
     // ---- a1: split; the residual goes straight to every destination (split-send)
-    const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
-#pragma unroll
-    for (int h = 0; h < (have_pre ? 0 : C::kIters); h += C::kBatch) {
-      uint4 v[C::kBatch];
-#pragma unroll
-      for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
-#pragma unroll
-      for (int i = 0; i < C::kBatch; ++i) {
-        const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;
-        if (DT == kF32) {
-          uint32_t s4, h4;
-          uint2 lo;
-          split4_f32(v[i], s4, lo, h4);
-          *reinterpret_cast<uint32_t *>(sym + e) = s4;
-          for (uint32_t d = 0; d < J.nd; ++d) {
-            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
-            *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
-          }
-        } else {
-          uint32_t s0, s1, r0, r1;
-          if (DT == kBF16) {
-            split4_bf16(v[i].x, v[i].y, s0, r0);
-            split4_bf16(v[i].z, v[i].w, s1, r1);
-          } else {
-            split4_f16(v[i].x, v[i].y, s0, r0);
-            split4_f16(v[i].z, v[i].w, s1, r1);
-          }
-          *reinterpret_cast<uint2 *>(sym + e) = make_uint2(s0, s1);
-          for (uint32_t d = 0; d < J.nd; ++d)
-            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(r0, r1);
-        }
-      }
-    }
+    split_block<DT, B, true, true>(J, g, b, src, buf);
     __syncwarp();
-
-    // ---- a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body);
-    // symbols and table entries of 8 rounds are loaded ahead of their math.
-    // Software pipeline (2-byte types): while this block is coded, the NEXT
-    // tile's block (prefetched ticket) is loaded kPF groups ahead and split
-    // into the symbol rows this block has already consumed, its residual
-    // leaving for its destinations at once -- no exposed load latency.
-    const EncJob *NJ = nullptr;
-    uint64_t nblk = 0;
-    if (DT != kF32 && next_it < P.n_e_items) {
-      const int nj = (int)(next_it % (uint64_t)P.ne);
-      const EncJob &Jn = P.e[nj];
-      const uint64_t nb = (next_it / (uint64_t)P.ne) * kTileBlocks + warp;
-      if (!Jn.raw && ((credit_done >> nj) & 1u) && nb < Jn.g.n_blocks) {
-        NJ = &Jn;
-        nblk = nb;
-        presplit = next_it;
-      }
-    }
-    constexpr int kGroups = C::kRounds / 8;
-    constexpr int kPF = 4;  // prefetch distance in 8-round groups (divides kGroups)
-    const uint8_t *nsrc = NJ ? NJ->in + nblk * (uint64_t)B * elem_bytes(DT) + 16 * lane : nullptr;
-    uint4 pre[kPF];
-    if (NJ) {
-#pragma unroll
-      for (int q = 0; q < kPF; ++q) pre[q] = ldg_nc_v4(nsrc + 512 * (kGroups - 1 - q));
-    }
-    const uint32_t lt = lanemask_lt();
-    uint32_t x = kL;
-    uint32_t wp = 0;
-    constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
-    constexpr int kG = 8;
-#pragma unroll 1
-    for (int k0 = kGroups - 1; k0 >= 0; k0 -= kPF) {
-#pragma unroll
-      for (int q = 0; q < kPF; ++q) {
-        const int k = k0 - q;  // group k = rounds 8k .. 8k+7
-        const int j0 = 8 * k + 7;
-        uint4 ent[kG];
-#pragma unroll
-        for (int u = 0; u < kG; ++u) ent[u] = tab[sym[(j0 - u) * 32 + lane]];
-#pragma unroll
-        for (int u = 0; u < kG; ++u) {
-          const uint4 e = ent[u];
-          const bool p = (x | 0x7FFFFu) >= e.y;
-          const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
-          // beyond kCap the block is stored raw anyway: clamp instead of branching
-          const uint32_t idx = min(wp + __popc(m & lt), kCap - 1);
-          if (p) blk16[64 + idx] = (uint16_t)x;
-          x = p ? (x >> 16) : x;
-          wp += __popc(m);
-          const uint32_t qq = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
-          x = x + e.z + qq * e.w;
-        }
-        if (NJ) {  // split the next block's group k into the rows just consumed
-          __syncwarp();
-          const uint4 v = pre[q];
-          if (k - kPF >= 0) pre[q] = ldg_nc_v4(nsrc + 512 * (k - kPF));
-          uint32_t s0, s1, r0, r1;
-          if (DT == kBF16) {
-            split4_bf16(v.x, v.y, s0, r0);
-            split4_bf16(v.z, v.w, s1, r1);
-          } else {
-            split4_f16(v.x, v.y, s0, r0);
-            split4_f16(v.z, v.w, s1, r1);
-          }
-          const uint32_t e = 256 * k + 8 * lane;
-          *reinterpret_cast<uint2 *>(sym + e) = make_uint2(s0, s1);
-          const StreamGeom &gn = NJ->g;
-          for (uint32_t d = 0; d < NJ->nd; ++d)
-            *reinterpret_cast<uint2 *>(NJ->dst[d] + gn.off_res0 + nblk * B + e) = make_uint2(r0, r1);
-        }
-      }
-    }
-    const uint32_t K = wp;
+    encode_block<DT, B, false>(J, g, 0, buf, tab, x, K, ovf);
     const uint32_t coded = (uint32_t)round16(128 + 2ull * K);
     raw = coded >= (uint32_t)B;  // stored raw (R13)
     size = raw ? (uint32_t)B : coded;
     kdir = raw ? kRawBlock : K;
-    if (!raw) {
-      blk32[lane] = x;
-      const uint32_t pad_words = (coded - 128 - 2 * K) / 2;
-      if ((uint32_t)lane < pad_words) blk16[64 + K + lane] = 0;
-    } else {
-      // stored raw: the payload is the block's symbols; `sym` may already hold
-      // the next block's, so split them again from the input into blk (rare path)
-      __syncwarp();
-      for (uint32_t v = lane; v < (uint32_t)(C::kIters * 32); v += 32) {
-        const uint4 w = ldg_nc_v4(src + 16 * (size_t)v);
-        const uint32_t e = v * C::kVec;
-        if (DT == kF32) {
-          uint32_t s4, h4;
-          uint2 lo;
-          split4_f32(w, s4, lo, h4);
-          *reinterpret_cast<uint32_t *>(blk + e) = s4;
-        } else {
-          uint32_t s0, s1, r0, r1;
-          if (DT == kBF16) {
-            split4_bf16(w.x, w.y, s0, r0);
-            split4_bf16(w.z, w.w, s1, r1);
-          } else {
-            split4_f16(w.x, w.y, s0, r0);
-            split4_f16(w.z, w.w, s1, r1);
-          }
-          *reinterpret_cast<uint2 *>(blk + e) = make_uint2(s0, s1);
-        }
-      }
+    __syncwarp();
+    if (raw) {
+      split_block<DT, B, false, false>(J, g, b, src, buf);  // payload = the symbols in element order
+    } else if (!ovf && lane < 8) {
+      buf16[K + lane] = 0;  // zero pad up to the 16-byte boundary (K + 8 <= kCap + 8 words fit)
     }
     __syncwarp();
   }
@@ -592,15 +558,34 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
   if (b < g.n_blocks) {
     unsigned long long off = tile_off;
     for (int w = 0; w < warp; ++w) off += S.size[w];
-    const uint4 *srcv = reinterpret_cast<const uint4 *>(blk);
     for (uint32_t d = 0; d < J.nd; ++d) {
-      uint8_t *o = J.dst[d];
+      uint8_t *o = J.dst[d] + g.off_pay + off;
       if (lane == 0) {
-        reinterpret_cast<uint32_t *>(o + g.off_dir)[b] = kdir;
-        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(o + g.off_coff)[b / g.CB] = off;
+        reinterpret_cast<uint32_t *>(J.dst[d] + g.off_dir)[b] = kdir;
+        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[b / g.CB] = off;
       }
-      uint4 *dstv = reinterpret_cast<uint4 *>(o + g.off_pay + off);
-      for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = srcv[i];
+      if (raw) {
+        for (uint32_t i = lane; i < size / 16; i += 32)
+          reinterpret_cast<uint4 *>(o)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      } else {
+        reinterpret_cast<uint32_t *>(o)[lane] = x;  // the block header: 32 final lane states
+        if (!ovf)
+          for (uint32_t i = lane; i < (size - 128) / 16; i += 32)
+            reinterpret_cast<uint4 *>(o + 128)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      }
+    }
+    if (ovf && !raw) {
+      // rare: the words outran the consumed symbol rows -- code the block again,
+      // now storing each word straight to its final place (offset known)
+      __syncwarp();
+      split_block<DT, B, false, true>(J, g, b, src, buf);
+      __syncwarp();
+      uint32_t x2 = kL, K2 = 0;
+      bool o2 = false;
+      encode_block<DT, B, true>(J, g, off, buf, tab, x2, K2, o2);
+      for (uint32_t d = 0; d < J.nd; ++d)
+        for (uint32_t i = 2 * K + lane * 2; i < size - 128; i += 64)
+          *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + i) = 0;
     }
     if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
   } else if (g.n_blocks == 0 && warp == 0) {  // no whole block: header + raw tail only
@@ -759,6 +744,27 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
   dec_done(J);
 }
 
+// Epilogue that folds a decoded source into the warp's fp32 accumulator (a9).
+struct FoldEpi {
+  float *acc;
+  bool first;
+  template <int DT>
+  __device__ __forceinline__ void apply(uint32_t e0, uint4 a, uint4 b) const {
+    float v[8];
+    if (!first)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = acc[e0 + i];
+    if (DT == kF32) {
+      fold_vec<DT>(v, a, first);
+      fold_vec<DT>(v + 4, b, first);
+    } else {
+      fold_vec<DT>(v, a, first);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[e0 + i] = v[i];
+  }
+};
+
 // ---------------------------------------------------------------- D item: decode + reduce (a9)
 template <int DT, int B>
 __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
@@ -827,6 +833,7 @@ __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
           for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
         }
       }
+      __syncwarp();
       continue;
     }
     const uint64_t key = (2ull << 62) | ((uint64_t)jidx << 48) | ((uint64_t)s << 40) | c;
@@ -853,36 +860,30 @@ __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
     if (b < g.n_blocks && !tb) {
       const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
       stage_payload(stream, g, off, size, pay);
-      const uint8_t *syms = pay;
+      FoldEpi epi{acc, first};
       if (K != kRawBlock) {
-        if (!rans_decode_warp<B>(pay, K, dtab, symb)) bad = true;
-        syms = symb;
-      }
-      __syncwarp();
-      // join + fold 8 (fp32: 4) elements per lane step
-      for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer) {
-        uint4 v;
-        if (DT == kF32) {
-          const uint32_t s4 = *reinterpret_cast<const uint32_t *>(syms + e);
-          const uint2 lo = ld_cg_v2(stream + g.off_res0 + 2 * (b * B + e));
-          const uint32_t h4 = ld_cg_u32c(stream + g.off_res1 + b * B + e);
-          v = join4_f32(s4, lo, h4);
-        } else {
-          const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
-          const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
-          if (DT == kBF16) {
-            join4_bf16(s8.x, r8.x, v.x, v.y);
-            join4_bf16(s8.y, r8.y, v.z, v.w);
+        if (!decode_join_warp_epi<DT, B>(pay, K, dtab, symb, stream, g, b, epi)) bad = true;
+      } else {  // stored-raw block: symbols are the payload
+        for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
+          const uint2 s8 = *reinterpret_cast<const uint2 *>(pay + e);
+          if (DT == kF32) {
+            const uint4 lo = ld_cg_v4(stream + g.off_res0 + 2 * (b * B + e));
+            const uint2 hi = ld_cg_v2(stream + g.off_res1 + b * B + e);
+            epi.template apply<DT>(e, join4_f32(s8.x, make_uint2(lo.x, lo.y), hi.x),
+                                   join4_f32(s8.y, make_uint2(lo.z, lo.w), hi.y));
           } else {
-            join4_f16(s8.x, r8.x, v.x, v.y);
-            join4_f16(s8.y, r8.y, v.z, v.w);
+            const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
+            uint4 v;
+            if (DT == kBF16) {
+              join4_bf16(s8.x, r8.x, v.x, v.y);
+              join4_bf16(s8.y, r8.y, v.z, v.w);
+            } else {
+              join4_f16(s8.x, r8.x, v.x, v.y);
+              join4_f16(s8.y, r8.y, v.z, v.w);
+            }
+            epi.template apply<DT>(e, v, v);
           }
         }
-        float a[8];
-        if (!first)
-          for (int i = 0; i < kPer; ++i) a[i] = acc[e + i];
-        fold_vec<DT>(a, v, first);
-        for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
       }
     }
     __syncwarp();
@@ -916,11 +917,11 @@ __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
 
 // ---------------------------------------------------------------- the kernel
 template <int DT, int B, bool RED>
-__global__ void __launch_bounds__(256, RED ? 1 : 3) k_fused(const __grid_constant__ Plan P) {
+__global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constant__ Plan P) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ FusedShared S;
   const int tid = threadIdx.x;
-  uint64_t enc_key = ~0ull, dec_key = ~0ull, presplit = ~0ull;
+  uint64_t enc_key = ~0ull, dec_key = ~0ull;
   uint32_t credit_done = 0;
   const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
   if (tid == 0) {
@@ -933,9 +934,7 @@ __global__ void __launch_bounds__(256, RED ? 1 : 3) k_fused(const __grid_constan
     if (tid == 0) S.tk[par ^ 1] = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
     if (it < ne) {
       const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
-      __syncthreads();  // the next ticket is visible: the encoder pre-splits that tile
-      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, it, S.tk[par ^ 1],
-                      presplit);
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done);
     } else if (it < ne + nc) {
       copy_item(P.c, it - ne);
     } else {
