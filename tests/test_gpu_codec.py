@@ -212,3 +212,25 @@ def test_c2_full_size_1gib_sampled(uz, orc):
         got = stream[sec["off_pay"] + offs[b]: sec["off_pay"] + offs[b] + sizes[b]].tobytes()
         assert got == ref, b
         assert np.array_equal(stream[sec["off_res0"] + b * B: sec["off_res0"] + (b + 1) * B], res.astype(np.uint8))
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+def test_encoder_word_overflow_rare_path(uz, orc, dtype):
+    """Blocks whose first-coded rounds (the high element indices, R-1 first) are
+    expensive but which still compress: the coded words outrun the symbol rows
+    the encoder has consumed, and the GPU encoder takes its rare path (words
+    stored straight to their final place).  Bytes must still equal the oracle."""
+    B = 4096
+    nb = 12
+    bits = synth.constant(nb * B + 3, 0x3F80 if dtype == BF16 else (0x3C00 if dtype == F16 else 0x3F800000),
+                          dtype).copy()
+    rnd = synth.random_bits(nb * B, 77, dtype)
+    for blk in range(nb):
+        hi = 96 + 2 * blk  # rounds >= hi are random, the rest constant
+        sl = slice(blk * B + hi * 32, (blk + 1) * B)
+        bits[sl] = rnd[sl]
+    ref = orc.compress(dtype, bits)
+    got = gpu_compress(uz, bits, dtype)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, bits.size, dtype)
+    assert st == 0 and np.array_equal(back, bits)
