@@ -205,16 +205,18 @@ __device__ bool wait_credit(const Plan &P, const unsigned long long *cr, uint32_
   }
 }
 
-// Decoupled look-back (one full warp) over the tiles of one stream; returns
-// the exclusive prefix of tile t, or ~0 on abort.
-__device__ unsigned long long lookback(const Plan &P, unsigned long long *status, uint64_t t,
-                                       unsigned long long agg) {
+// Decoupled look-back over the tiles of one stream, in two halves so the
+// aggregate can be published as soon as a tile is coded and the scan finished
+// later.  publish: one thread.  finish: one full warp; returns the exclusive
+// prefix of tile t, or ~0 on abort.
+__device__ __forceinline__ void lookback_publish(unsigned long long *status, uint64_t t, unsigned long long agg) {
+  st_relaxed_u64(&status[t], (t == 0 ? kFlagInc : kFlagAgg) | agg);
+}
+
+__device__ unsigned long long lookback_finish(const Plan &P, unsigned long long *status, uint64_t t,
+                                              unsigned long long agg) {
   const int lane = threadIdx.x & 31;
-  if (t == 0) {
-    if (lane == 0) st_relaxed_u64(&status[0], kFlagInc | agg);
-    return 0;
-  }
-  if (lane == 0) st_relaxed_u64(&status[t], kFlagAgg | agg);
+  if (t == 0) return 0;
   unsigned long long excl = 0, t0 = 0;
   int64_t base = (int64_t)t - 1;
   for (int spin = 0;; ++spin) {
@@ -248,6 +250,12 @@ __device__ unsigned long long lookback(const Plan &P, unsigned long long *status
   }
   if (lane == 0) st_relaxed_u64(&status[t], kFlagInc | (excl + agg));
   return excl;
+}
+
+__device__ unsigned long long lookback(const Plan &P, unsigned long long *status, uint64_t t,
+                                       unsigned long long agg) {
+  if ((threadIdx.x & 31) == 0) lookback_publish(status, t, agg);
+  return lookback_finish(P, status, t, agg);
 }
 
 // ---------------------------------------------------------------- fp32 fold helpers (a9, R11)
@@ -306,8 +314,9 @@ struct FusedCfg {
   static constexpr int kWarpBuf = B + 256;                  // per warp: symbols/words (E) or payload + ring (D)
   static constexpr int kDecTab = 4096 * 4;
   static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce)
+  static constexpr int ring(bool red) { return red ? 0 : 16384; }  // coded tile awaiting its offset
   static constexpr int smem(bool dec, bool red) {
-    return kEncTab + kWarps * kWarpBuf + (dec ? kDecTab : 0) + (red ? kWarps * kAcc : 0);
+    return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0) + (red ? kWarps * kAcc : 0);
   }
 };
 
@@ -316,7 +325,9 @@ struct FusedShared {
   uint32_t abort;
   uint32_t tile_cnt;
   unsigned long long tile_off;
-  uint32_t size[kWarps], k[kWarps];
+  uint32_t size[kWarps], k[kWarps], ovf[kWarps];
+  uint32_t psize[kWarps], pkdir[kWarps];  // the pending (coded, offset unknown) tile
+  unsigned long long pagg, ptile_off;
   unsigned long long prefix;
   unsigned long long src_off[kMaxRanks];
   unsigned long long src_payload[kMaxRanks];
@@ -370,11 +381,14 @@ __device__ void finalize_stream(const EncJob &J, unsigned long long payload) {
 // (R-1-j)*32, lanes in order within a row) for the encoder; otherwise element
 // order (the stored-raw payload).  RES: also store the residual plane(s) to
 // every destination (split-send: they leave before the exponents are coded).
-template <int DT, int B, bool RES, bool REV>
-__device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
-                                            uint8_t *buf) {
+template <int DT, int B, bool RES, bool REV, bool ND1>
+__device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
+                                              uint8_t *buf) {
   using C = FusedCfg<DT, B>;
   const int lane = threadIdx.x & 31;
+  // ND1: one destination (codec, P2P): the residual bases are computed once
+  uint8_t *r0 = J.dst[0] + g.off_res0 + (DT == kF32 ? 2 : 1) * (b * B);
+  uint8_t *r1 = J.dst[0] + g.off_res1 + b * B;
 #pragma unroll
   for (int h = 0; h < C::kIters; h += C::kBatch) {
     uint4 v[C::kBatch];
@@ -389,27 +403,45 @@ __device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g
         uint2 lo;
         split4_f32(v[i], s4, lo, h4);
         *reinterpret_cast<uint32_t *>(buf + pos) = s4;
-        if (RES)
-          for (uint32_t d = 0; d < J.nd; ++d) {
-            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
-            *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
+        if (RES) {
+          if (ND1) {
+            *reinterpret_cast<uint2 *>(r0 + 2 * e) = lo;
+            *reinterpret_cast<uint32_t *>(r1 + e) = h4;
+          } else {
+            for (uint32_t d = 0; d < J.nd; ++d) {
+              *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
+              *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
+            }
           }
+        }
       } else {
-        uint32_t s0, s1, r0, r1;
+        uint32_t s0, s1, q0, q1;
         if (DT == kBF16) {
-          split4_bf16(v[i].x, v[i].y, s0, r0);
-          split4_bf16(v[i].z, v[i].w, s1, r1);
+          split4_bf16(v[i].x, v[i].y, s0, q0);
+          split4_bf16(v[i].z, v[i].w, s1, q1);
         } else {
-          split4_f16(v[i].x, v[i].y, s0, r0);
-          split4_f16(v[i].z, v[i].w, s1, r1);
+          split4_f16(v[i].x, v[i].y, s0, q0);
+          split4_f16(v[i].z, v[i].w, s1, q1);
         }
         *reinterpret_cast<uint2 *>(buf + pos) = make_uint2(s0, s1);
-        if (RES)
-          for (uint32_t d = 0; d < J.nd; ++d)
-            *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(r0, r1);
+        if (RES) {
+          if (ND1) {
+            *reinterpret_cast<uint2 *>(r0 + e) = make_uint2(q0, q1);
+          } else {
+            for (uint32_t d = 0; d < J.nd; ++d)
+              *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(q0, q1);
+          }
+        }
       }
     }
   }
+}
+
+template <int DT, int B, bool RES, bool REV>
+__device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
+                                            uint8_t *buf) {
+  if (!RES || J.nd == 1) split_block_t<DT, B, RES, REV, true>(J, g, b, src, buf);
+  else split_block_t<DT, B, RES, REV, false>(J, g, b, src, buf);
 }
 
 // a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body); the
@@ -463,12 +495,74 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
   ovf = over;
 }
 
+// A coded tile whose payload waits in the CTA's ring for its offset: the
+// tile's aggregate is published as soon as it is coded, the look-back is
+// finished one tile later (when every predecessor has long been coded), so
+// warps never idle on stragglers.  Uniform across the CTA.
+struct EncPending {
+  int32_t job;  // -1: none
+  uint64_t t;
+};
+
+template <int DT, int B>
+__device__ void resolve_pending(const Plan &P, FusedShared &S, const uint8_t *ring, EncPending &pd) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const EncJob &J = P.e[pd.job];
+  const StreamGeom &g = J.g;
+  const uint64_t t = pd.t;
+  pd.job = -1;
+  if (warp == 0) {
+    const unsigned long long excl = lookback_finish(P, J.tile_status, t, S.pagg);
+    if (lane == 0) S.ptile_off = excl;
+  }
+  __syncthreads();
+  const unsigned long long tile_off = S.ptile_off;
+  if (tile_off != ~0ull) {
+    const uint64_t b0 = t * kTileBlocks, b = b0 + warp;
+    const uint64_t c = b0 / g.CB;
+    uint32_t roff = 0;
+    for (int w = 0; w < warp; ++w) roff += S.psize[w];
+    const uint32_t size = S.psize[warp];
+    if (b < g.n_blocks) {
+      const unsigned long long off = tile_off + roff;
+      for (uint32_t d = 0; d < J.nd; ++d) {
+        if (lane == 0) {
+          reinterpret_cast<uint32_t *>(J.dst[d] + g.off_dir)[b] = S.pkdir[warp];
+          if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[b / g.CB] = off;
+        }
+        uint4 *o = reinterpret_cast<uint4 *>(J.dst[d] + g.off_pay + off);
+        for (uint32_t i = lane; i < size / 16; i += 32) o[i] = reinterpret_cast<const uint4 *>(ring + roff)[i];
+      }
+      if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
+    }
+    if (b0 % g.CB == 0 && warp == kWarps - 1) {  // the chunk's first tile carries its table
+      const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
+      for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
+    }
+    bool flags = false;
+    for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+    if (flags) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_system();
+        if (atomicAdd(&S.tile_cnt, 1u) == kWarps - 1) {
+          S.tile_cnt = 0;
+          const unsigned long long off16 = tile_off >> 4;
+          for (uint32_t d = 0; d < J.nd; ++d)
+            if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+        }
+      }
+    }
+  }
+  __syncthreads();  // the ring and the pending sizes are free again
+}
+
 // One encode tile: every warp codes one block; one warp finds the tile's
 // offset by decoupled look-back over tiles; the last warp of the tile to
 // finish its stores releases the tile's flags.
 template <int DT, int B>
 __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &enc_key, uint32_t &credit_done) {
+                         uint64_t &enc_key, uint32_t &credit_done, uint8_t *ring, int ring_bytes, EncPending &pd) {
   using C = FusedCfg<DT, B>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
@@ -541,14 +635,47 @@ __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, u
     }
     __syncwarp();
   }
-  if (lane == 0) S.size[warp] = size;
+  if (lane == 0) {
+    S.size[warp] = size;
+    S.ovf[warp] = (ovf && !raw) ? 1u : 0u;
+  }
   __syncthreads();
+  if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);  // the previous tile's offset is due now
 
-  // ---- a5: tile prefix by decoupled look-back (one warp per tile)
+  // ---- a5: tile prefix by decoupled look-back
+  uint32_t sum = 0, roff = 0, anyovf = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) roff += S.size[w];
+    sum += S.size[w];
+    anyovf |= S.ovf[w];
+  }
+  if (g.n_blocks && !anyovf && sum <= (uint32_t)ring_bytes) {
+    // park the coded tile in the ring, publish its aggregate, go on coding
+    if (b < g.n_blocks) {
+      uint8_t *r = ring + roff;
+      if (raw) {
+        for (uint32_t i = lane; i < size / 16; i += 32)
+          reinterpret_cast<uint4 *>(r)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      } else {
+        reinterpret_cast<uint32_t *>(r)[lane] = x;
+        for (uint32_t i = lane; i < (size - 128) / 16; i += 32)
+          reinterpret_cast<uint4 *>(r + 128)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      }
+    }
+    if (lane == 0) {
+      S.psize[warp] = size;
+      S.pkdir[warp] = kdir;
+    }
+    if (tid == 0) {
+      S.pagg = sum;
+      lookback_publish(J.tile_status, t, sum);
+    }
+    pd.job = jidx;
+    pd.t = t;
+    return;  // the item-end barrier publishes the ring contents to the resolving warps
+  }
   if (warp == 0) {
-    unsigned long long agg = lane < kWarps ? S.size[lane] : 0u;
-    agg = warp_sum_u64(agg);
-    const unsigned long long excl = lookback(P, J.tile_status, t, agg);
+    const unsigned long long excl = lookback(P, J.tile_status, t, sum);
     if (lane == 0) S.tile_off = excl;
   }
   __syncthreads();
@@ -683,7 +810,7 @@ __device__ __forceinline__ void stage_payload(const uint8_t *stream, const Strea
 }
 
 // ---------------------------------------------------------------- D item: decode (+ join)
-template <int DT, int B>
+template <int DT, int B, bool RED>
 __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
                          uint64_t &dec_key) {
   using C = FusedCfg<DT, B>;
@@ -708,7 +835,7 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
     dec_done(J);
     return;
   }
-  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf);
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(RED));
   if (g.n_blocks && need_table) {
     if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
       if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
@@ -814,8 +941,8 @@ __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
   const uint64_t b0 = t * kTileBlocks;
   const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
   const uint64_t b = b0 + warp;
-  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf);
-  float *acc = reinterpret_cast<float *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::kDecTab) + warp * B;
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true));
+  float *acc = reinterpret_cast<float *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true) + C::kDecTab) + warp * B;
   uint8_t *pay = smem + C::kEncTab + warp * C::kWarpBuf;
   uint8_t *symb = pay + B;
   bool bad = false;
@@ -923,6 +1050,9 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
   const int tid = threadIdx.x;
   uint64_t enc_key = ~0ull, dec_key = ~0ull;
   uint32_t credit_done = 0;
+  using Cf = FusedCfg<DT, B>;
+  uint8_t *ring = smem + Cf::kEncTab + kWarps * Cf::kWarpBuf;
+  EncPending pd{-1, 0};
   const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
   if (tid == 0) {
     S.tile_cnt = 0;
@@ -932,9 +1062,11 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
   uint64_t it = S.tk[0];
   for (int par = 0; it < total; par ^= 1) {
     if (tid == 0) S.tk[par ^ 1] = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
+    const bool coded_e = it < ne && !P.e[it % (uint64_t)P.ne].raw;
+    if (pd.job >= 0 && !coded_e) resolve_pending<DT, B>(P, S, ring, pd);
     if (it < ne) {
       const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
-      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done);
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, ring, Cf::ring(RED), pd);
     } else if (it < ne + nc) {
       copy_item(P.c, it - ne);
     } else {
@@ -942,11 +1074,12 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
       int j = 0;
       while (j + 1 < P.nd_jobs && k >= P.d[j].ntiles) k -= P.d[j++].ntiles;
       if (RED && P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
-      else dec_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
+      else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key);
     }
     __syncthreads();
     it = S.tk[par ^ 1];
   }
+  if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);
   if (tid == 0) {  // the last CTA out resets the ticket for the next launch
     __threadfence();
     if (atomicAdd(P.ticket + 1, 1u) == gridDim.x - 1) {
