@@ -21,6 +21,15 @@ import torch.distributed as dist
 GB = 1e9
 
 
+SMOKE = os.environ.get("UZIP_BENCH_SMOKE") == "1"  # 2 ranks on one GPU over gloo: code-path check only
+
+
+def _max_over_ranks(v: float) -> float:
+    t = torch.tensor([v], device="cpu" if SMOKE else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _timed(fn, stream, steps, warmup, group=None):
     for _ in range(warmup):
         fn()
@@ -33,10 +42,9 @@ def _timed(fn, stream, steps, warmup, group=None):
         fn()
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+    ms = _max_over_ranks(e0.elapsed_time(e1))
     dist.barrier(group)
-    return float(ms.item()) / steps
+    return ms / steps
 
 
 def run(args):
@@ -45,12 +53,17 @@ def run(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SMOKE else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if SMOKE:
+        dist.init_process_group("gloo")
+        args.bytes = min(args.bytes, 8 << 20)
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     uz.build() if rank == 0 else None
     dist.barrier()
-    comm = uz.Comm.from_group(None, local)
+    comm = uz.Comm.from_group(None, local, **(dict(staging_bytes=32 << 20, max_ctas=16, poll_timeout_ms=60000)
+                                              if SMOKE else {}))
     stream = torch.cuda.Stream()
     n = args.bytes // 2
     g = torch.Generator(device="cuda")
@@ -80,16 +93,43 @@ def run(args):
     assert comm.async_error() == 0
     st = comm.stats() if role == "send" else None
     # correctness spot check: receiver sees the sender's bytes
-    ref = torch.empty_like(x)
     if role == "send":
-        dist.send(x, peer)
+        dist.send(x.cpu() if SMOKE else x, peer)
     elif role == "recv":
+        ref = torch.empty(x.shape, dtype=x.dtype, device="cpu" if SMOKE else x.device)
         dist.recv(ref, peer)
-        assert torch.equal(ref.view(torch.int16), y.view(torch.int16)), "P2P mismatch"
-    ms_nccl = _timed(nccl_step, stream, args.steps, args.warmup)
+        assert torch.equal(ref.view(torch.int16).cpu(), y.view(torch.int16).cpu()), "P2P mismatch"
+    ms_nccl = float("nan") if SMOKE else _timed(nccl_step, stream, args.steps, args.warmup)
+
+    # e2e through the public API with host buffers: the sender copies its input from pinned host memory
+    # and sends; the receiver receives and reads 16 bytes of the result back; wall clock, max over ranks
+    host = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+    if role == "send":
+        host.copy_(x.cpu())
+    xd = torch.empty_like(x)
+    res_h = torch.empty(8, dtype=torch.int16, pin_memory=True)
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            if role == "send":
+                xd.copy_(host, non_blocking=True)
+                comm.send(xd, peer, stream)
+            elif role == "recv":
+                comm.recv(y, peer, stream)
+                res_h.copy_(y[:8].view(torch.int16), non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(args.warmup):
+        e2e_step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = _max_over_ranks(time.perf_counter() - t0) / args.steps
+    dist.barrier()
 
     # allreduce 256 MiB activations (two-shot compressed) vs NCCL
-    T = (256 << 20) // (2 * 4096)
+    T = ((8 if SMOKE else 256) << 20) // (2 * 4096)
     ga = torch.Generator(device="cuda")
     ga.manual_seed(3000 + rank)
     scale = torch.exp(torch.randn(4096, device="cuda", generator=ga) * 0.5)
@@ -107,7 +147,7 @@ def run(args):
 
     ms_ar = _timed(ar_step, stream, args.steps, args.warmup)
     ar_stats = comm.stats()
-    ms_ar_nccl = _timed(ar_nccl, stream, args.steps, args.warmup)
+    ms_ar_nccl = float("nan") if SMOKE else _timed(ar_nccl, stream, args.steps, args.warmup)
     assert comm.async_error() == 0
 
     sts = [None] * world
@@ -131,6 +171,8 @@ def run(args):
                          "achieved": round(wire_gbs, 1), "peak": 770.0, "unit": "GB/s",
                          "peak_source": "B200_PROFILING.md measured peer copy per direction",
                          "frac": round(wire_gbs / 770.0, 4), "traffic": None},
+            "e2e": {"value": round(raw / e2e_s / GB, 3), "unit": "GB/s", "h2d_bytes_per_step": pairs * 2 * n,
+                    "d2h_bytes_per_step": pairs * 16, "ms_per_step": round(e2e_s * 1e3, 3)},
             "clocks": clk.summary(),
             "gpu_launches": args.steps * 2 * 2 * max(1, (2 * n) // (256 << 20)),
         }

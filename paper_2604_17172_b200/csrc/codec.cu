@@ -63,13 +63,13 @@ __device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256, 3) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
+__global__ void __launch_bounds__(256, 4) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
                                                   uint8_t *__restrict__ out, uint64_t n, CodecWs ws,
                                                   int32_t *__restrict__ d_status) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t *dtab = reinterpret_cast<uint32_t *>(smem);
   uint32_t *soff = reinterpret_cast<uint32_t *>(smem + DecShared::kTab);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   uint8_t *pay = smem + DecShared::kTab + DecShared::kOff + warp * DecShared::kWarpBuf;
   uint8_t *ring = pay + kMaxB;
 

@@ -22,7 +22,7 @@ __device__ __forceinline__ uint32_t block_size(uint32_t d, uint32_t B, bool &bad
 // Decode table of one chunk: f:12 <<20 | (slot-cdf):12 <<8 | sym:8 (a7).
 // All 256 threads; returns false (uniformly) if the table is invalid.
 __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const uint32_t f = ld_cg_u16(ft + tid);
   uint32_t incl = f;
   for (int o = 1; o < 32; o <<= 1) {

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ P
   const EncJob &J = P.e[blockIdx.y];
   if (J.raw) return;
   const StreamGeom &g = J.g;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const uint32_t c = blockIdx.x;
 
   // reset the look-back words of this job for the k_fused launch that follows
@@ -506,7 +506,7 @@ struct EncPending {
 
 template <int DT, int B>
 __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint8_t *ring, EncPending &pd) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const EncJob &J = P.e[pd.job];
   const StreamGeom &g = J.g;
   const uint64_t t = pd.t;
@@ -564,7 +564,7 @@ template <int DT, int B>
 __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
                          uint64_t &enc_key, uint32_t &credit_done, uint8_t *ring, int ring_bytes, EncPending &pd) {
   using C = FusedCfg<DT, B>;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
     if (tid == 0) {
       uint32_t ok = 1;
@@ -814,7 +814,7 @@ template <int DT, int B, bool RED>
 __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
                          uint64_t &dec_key) {
   using C = FusedCfg<DT, B>;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = warp_id();
   const StreamGeom &g = J.g;
   const uint64_t b0 = t * kTileBlocks;
   const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
@@ -835,7 +835,7 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
     dec_done(J);
     return;
   }
-  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(RED));
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + P.ring_bytes);
   if (g.n_blocks && need_table) {
     if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
       if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
@@ -897,7 +897,7 @@ template <int DT, int B>
 __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
                          uint64_t &dec_key) {
   using C = FusedCfg<DT, B>;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const StreamGeom &g = J.g;
   const uint32_t eb = elem_bytes(DT);
   constexpr int kPer = C::kVec;
@@ -1059,14 +1059,14 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
     S.tk[0] = atomicAdd(P.ticket, 1u);
   }
   __syncthreads();
-  uint64_t it = S.tk[0];
+  uint64_t it = uniform_u64(S.tk[0]);
   for (int par = 0; it < total; par ^= 1) {
     if (tid == 0) S.tk[par ^ 1] = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
     const bool coded_e = it < ne && !P.e[it % (uint64_t)P.ne].raw;
     if (pd.job >= 0 && !coded_e) resolve_pending<DT, B>(P, S, ring, pd);
     if (it < ne) {
       const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
-      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, ring, Cf::ring(RED), pd);
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, ring, P.ring_bytes, pd);
     } else if (it < ne + nc) {
       copy_item(P.c, it - ne);
     } else {
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
       else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key);
     }
     __syncthreads();
-    it = S.tk[par ^ 1];
+    it = uniform_u64(S.tk[par ^ 1]);
   }
   if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);
   if (tid == 0) {  // the last CTA out resets the ticket for the next launch
@@ -1114,13 +1114,16 @@ cudaError_t launch_tables_t(const Plan &p, cudaStream_t st) {
 }
 
 template <int DT, int B, bool RED>
-cudaError_t launch_fused_t(const Plan &p, cudaStream_t st, int max_ctas) {
+cudaError_t launch_fused_t(Plan p, cudaStream_t st, int max_ctas) {
   using C = FusedCfg<DT, B>;
   const bool dec = p.n_d_items > 0;
-  const int smem = C::smem(dec || RED, RED);
+  // the ring parks coded tiles (encode launches only; none in the reduce variant)
+  p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
+  const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0) +
+                   (RED ? kWarps * C::kAcc : 0);
   auto kern = k_fused<DT, B, RED>;
   static int attr_set = 0;
-  if (attr_set < smem) {
+  if (attr_set < C::smem(true, RED)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(true, RED));
     attr_set = C::smem(true, RED);
   }

@@ -80,6 +80,7 @@ struct Plan {
   uint32_t *ticket;                         // self-resetting ticket + exit counter (2 words)
   uint32_t *err;                            // sticky async error word
   uint64_t timeout_ns;
+  int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
 };
 
 // Workspace of one encode job: enc entries, serialized tables, look-back

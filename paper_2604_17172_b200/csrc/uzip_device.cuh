@@ -210,6 +210,14 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
   return v;
 }
+// Warp index as a value the compiler can prove warp-uniform (a broadcast), so
+// warp-collective code under warp-indexed control flow compiles to plain
+// VOTE/SHFL instead of WARPSYNC.COLLECTIVE sequences (measured in SASS).
+__device__ __forceinline__ int warp_id() { return __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0); }
+__device__ __forceinline__ uint64_t uniform_u64(uint64_t v) {
+  const uint32_t lo = __shfl_sync(0xFFFFFFFFu, (uint32_t)v, 0), hi = __shfl_sync(0xFFFFFFFFu, (uint32_t)(v >> 32), 0);
+  return ((uint64_t)hi << 32) | lo;
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));

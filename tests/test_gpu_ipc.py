@@ -20,3 +20,18 @@ def test_ipc_two_processes_same_gpu():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "rank 0 ok" in r.stdout and "rank 1 ok" in r.stdout
+
+
+def test_bench_dist_smoke_two_processes_same_gpu():
+    """bench.py's N > 1 leg (bench_dist.py) end to end, 2 ranks time-sliced on one GPU over gloo."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    env = dict(os.environ, UZIP_BENCH_SMOKE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "2", "--warmup", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["compression_ratio"] < 0.75
