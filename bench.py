@@ -107,8 +107,8 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def cpu_baseline(sample_bytes: int = 16 << 20, seed: int = 1001):
-    """The oracle as it stands (single thread) on a bounded sample of the W input."""
+def cpu_baseline(sample_bytes: int = 1 << 30, seed: int = 1001):
+    """The oracle as it stands (single thread) on the same 1 GiB W workload (~7-10 s of CPU work)."""
     import numpy as np
     import oracle
     import synth
@@ -134,7 +134,7 @@ def reference_arm(args):
     import oracle
     import synth
     oracle.build()
-    sample = 8 << 20
+    sample = 64 << 20
     n = sample // 2
     bits = synth.weights(n, 1001)
     for _ in range(args.warmup):
@@ -247,6 +247,7 @@ def run_codec(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_codec_e2e(uz, x, args, stream)
+    loop = run_loopback_p2p(uz, x, args)
 
     line = {
         "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",
@@ -262,6 +263,7 @@ def run_codec(args):
                      "peak_source": src, "unit": "GB/s", "frac": round(dom[1] / hbm, 4), "traffic": None,
                      "algorithmic_bytes_per_launch": dom[2]},
         "torch_copy_GBps": round(copy_gbs, 1),
+        "loopback_p2p": loop,
         "clocks": clk.summary(),
         "gpu_launches": 3 * args.steps,
     }
@@ -270,6 +272,41 @@ def run_codec(args):
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
+
+
+def run_loopback_p2p(uz, x, args):
+    """Context (not the headline): the full split-send path -- uzip_send on rank 0 and uzip_recv on
+    rank 1 -- with both ranks on this one GPU (loopback communicators), each persistent kernel capped
+    at half the SM slots.  Sender and receiver share the SMs and HBM, so this is a lower bound for
+    the NVLink case; the bytes still go through staging, tile flags and credits."""
+    import torch
+    comms = uz.Comm.init_all(2, [0, 0], max_ctas=2 * 148, staging_bytes=1 << 30)
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    y = torch.empty_like(x)
+
+    def step():
+        s1.wait_stream(s0)
+        comms[0].send(x, 1, s0)
+        comms[1].recv(y, 0, s1)
+        s0.wait_stream(s1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s0)
+    for _ in range(args.steps):
+        step()
+    e1.record(s0)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    ok = torch.equal(x.view(torch.int16), y.view(torch.int16)) and comms[0].async_error() == 0
+    st = comms[0].stats()
+    for c in comms:
+        c.destroy()
+    return {"value": round(x.numel() * 2 / (ms / 1e3) / GB, 2), "unit": "GB/s", "ms": round(ms, 4),
+            "bit_exact": bool(ok), "wire_ratio": round(st["wire_bytes"] / max(1, st["raw_bytes"]), 5),
+            "note": "sender+receiver kernels share one GPU (loopback), 1 GiB bf16 W"}
 
 
 def run_codec_e2e(uz, x, args, stream):
