@@ -170,6 +170,15 @@ UZIP_API uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, s
 UZIP_API uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype,
                              uzip_op_t op, uzip_comm_t comm, void *stream);
 
+/* Broadcast (RL weight sync, BASELINE configs[2]): after the call every rank's `buf`
+ * holds the root's `count` elements.  Compressed messages (>= the threshold, >= 3 ranks) use a
+ * compressed scatter + relay: the root encodes N-1 pieces once and sends piece k to receiver k
+ * (root egress r*S instead of (N-1)*r*S); each receiver forwards the compressed bytes of its piece
+ * to the other receivers without re-encoding, and decodes all pieces.  Otherwise the root's stream
+ * (or raw bytes) is fanned out to every receiver. */
+UZIP_API uzip_status_t uzip_broadcast(void *buf, size_t count, uzip_dtype_t dtype, int root, uzip_comm_t comm,
+                                      void *stream);
+
 /* First asynchronous error seen by the communicator's kernels (sync read). */
 UZIP_API uzip_status_t uzip_comm_get_async_error(uzip_comm_t comm, uzip_status_t *err);
 

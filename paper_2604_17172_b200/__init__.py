@@ -37,7 +37,7 @@ EXPORTED = [
     "uzip_compress_bound", "uzip_workspace_bytes", "uzip_workspace_init", "uzip_compress", "uzip_decompress",
     "uzip_comm_init", "uzip_comm_init_all", "uzip_comm_destroy", "uzip_send", "uzip_recv", "uzip_allgather",
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
-    "uzip_status_string", "uzip_version", "uzip_comm_read_staging",
+    "uzip_status_string", "uzip_version", "uzip_comm_read_staging", "uzip_broadcast",
 ]
 
 
@@ -103,6 +103,7 @@ def lib() -> ctypes.CDLL:
             l.uzip_comm_get_async_error.argtypes = [vp, ctypes.POINTER(i32)]
             l.uzip_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
             l.uzip_comm_read_staging.argtypes = [vp, i32, i32, vp, sz]
+            l.uzip_broadcast.argtypes = [vp, sz, i32, i32, vp, vp]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
@@ -329,6 +330,10 @@ class Comm:
         inp = out if inp is None else inp
         _check(lib().uzip_allreduce(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), out.numel(),
                                     uz_dtype(out.dtype), SUM, self.h, _stream(stream)), "uzip_allreduce")
+
+    def broadcast(self, t: torch.Tensor, root: int, stream=None):
+        _check(lib().uzip_broadcast(ctypes.c_void_p(t.data_ptr()), t.numel(), uz_dtype(t.dtype), root, self.h,
+                                    _stream(stream)), "uzip_broadcast")
 
     def async_error(self) -> int:
         e = ctypes.c_int(0)

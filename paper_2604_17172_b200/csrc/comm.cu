@@ -237,6 +237,22 @@ void dec_job(uzip_comm *c, Plan &p, int j, int dt, uint64_t n, bool compressed, 
   p.nd_jobs = j + 1;
 }
 
+// Relay destinations of decode job j (broadcast): the received stream is also
+// stored into `dsts`' staging for src = this rank (one round on each channel).
+void fwd_setup(uzip_comm *c, Plan &p, int j, const std::vector<int> &dsts) {
+  DecJob &J = p.d[j];
+  J.nfwd = (uint32_t)dsts.size();
+  for (size_t i = 0; i < dsts.size(); ++i) {
+    const int d = dsts[i];
+    const uint32_t q = c->send_seq[d]++;
+    const int slot = q & 1;
+    J.fdst[i] = c->peer[d] + c->L.stage(c->rank, slot);
+    J.fflag[i] = reinterpret_cast<unsigned long long *>(c->peer[d] + c->L.flags(c->rank, slot));
+    J.fcredit[i] = reinterpret_cast<const unsigned long long *>(c->region + c->L.credit(d, slot));
+    J.fepoch[i] = q + 1;
+  }
+}
+
 uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
   for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
   for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += p.d[j].ntiles;
@@ -529,6 +545,79 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
   c->nested = 0;
   c->cfg.min_compress_bytes = saved;
   return s;
+}
+
+uzip_status_t uzip_broadcast(void *buf, size_t count, uzip_dtype_t dtype, int root, uzip_comm_t c, void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (root < 0 || root >= c->nranks) return UZIP_ERR_INVALID_ARG;
+  if (count == 0 || c->nranks == 1) return UZIP_OK;
+  if (!buf || !aligned16(buf)) return UZIP_ERR_INVALID_ARG;
+  const int dt = (int)dtype;
+  const uint32_t eb = elem_bytes(dt);
+  const int N = c->nranks, me = c->rank;
+  const uint64_t msg = count * eb;
+  const bool comp = compress_message(c, msg);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t *b = static_cast<uint8_t *>(buf);
+  std::vector<int> rcv;  // receivers in rank order
+  for (int r = 0; r < N; ++r)
+    if (r != root) rcv.push_back(r);
+  if (!comp || N == 2) {
+    // fan-out: the root's one stream (or raw bytes) is stored to every receiver
+    if (uzip_status_t s2 = begin_call(c, me == root ? (uint64_t)(N - 1) * msg : 0, comp, st)) return s2;
+    const uint64_t per = round_elems(c, dt, comp, count, nullptr);
+    for (uint64_t o = 0; o < count; o += per) {
+      const uint64_t n = std::min<uint64_t>(per, count - o);
+      Plan p;
+      base_plan(c, p, dt);
+      if (me == root) enc_job(c, p, 0, dt, b + o * eb, n, comp, rcv);
+      else dec_job(c, p, 0, dt, n, comp, {root}, -1, nullptr, b + o * eb);
+      if (uzip_status_t s2 = launch(c, p, comp, st)) return s2;
+    }
+    return UZIP_OK;
+  }
+  // compressed scatter + relay (SURVEY 8(e) weight sync): piece k goes root -> rcv[k] once, rcv[k]
+  // forwards the compressed bytes to the other receivers; every receiver decodes every piece.
+  const int R = N - 1;
+  uint64_t P = (count + R - 1) / R;
+  P = (P + 7) & ~7ull;  // 16-byte aligned pieces
+  auto piece_len = [&](int k) -> uint64_t {
+    const uint64_t lo = std::min<uint64_t>(count, (uint64_t)k * P), hi = std::min<uint64_t>(count, lo + P);
+    return hi - lo;
+  };
+  int mine = -1;
+  for (int k = 0; k < R; ++k)
+    if (rcv[k] == me) mine = k;
+  const uint64_t egress = me == root ? msg : (uint64_t)(R - 1) * piece_len(mine) * eb;
+  if (uzip_status_t s2 = begin_call(c, egress, comp, st)) return s2;
+  const uint64_t per = round_elems(c, dt, comp, P, nullptr);
+  for (uint64_t o = 0; o < P; o += per) {
+    Plan p;
+    base_plan(c, p, dt);
+    auto part = [&](int k) -> uint64_t { const uint64_t L = piece_len(k); return L > o ? std::min(per, L - o) : 0; };
+    if (me == root) {
+      int j = 0;
+      for (int k = 0; k < R; ++k)
+        if (const uint64_t n = part(k)) enc_job(c, p, j++, dt, b + ((uint64_t)k * P + o) * eb, n, comp, {rcv[k]});
+    } else {
+      int j = 0;
+      if (const uint64_t n = part(mine)) {
+        dec_job(c, p, j, dt, n, comp, {root}, -1, nullptr, b + ((uint64_t)mine * P + o) * eb);
+        std::vector<int> hops;
+        for (int k = 0; k < R; ++k)
+          if (k != mine) hops.push_back(rcv[k]);
+        fwd_setup(c, p, j, hops);
+        ++j;
+      }
+      for (int k = 0; k < R; ++k)
+        if (k != mine)
+          if (const uint64_t n = part(k)) dec_job(c, p, j++, dt, n, comp, {rcv[k]}, -1, nullptr,
+                                                  b + ((uint64_t)k * P + o) * eb);
+    }
+    if (uzip_status_t s2 = launch(c, p, comp, st)) return s2;
+  }
+  return UZIP_OK;
 }
 
 uzip_status_t uzip_comm_get_async_error(uzip_comm_t c, uzip_status_t *err) {

@@ -809,10 +809,86 @@ __device__ __forceinline__ void stage_payload(const uint8_t *stream, const Strea
   __syncwarp();
 }
 
+// Copy stream bytes [o, o+len) from the local staging to the same offset in
+// every forward destination (all threads of the CTA).
+__device__ __forceinline__ void fwd_range(const DecJob &J, const uint8_t *stream, uint64_t o, uint64_t len) {
+  const uint64_t nv = len / 16;
+  for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    const uint4 v = ld_cg_v4(stream + o + 16 * i);
+    for (uint32_t d = 0; d < J.nfwd; ++d) *reinterpret_cast<uint4 *>(J.fdst[d] + o + 16 * i) = v;
+  }
+  for (uint64_t i = nv * 16 + threadIdx.x; i < len; i += blockDim.x) {
+    const uint8_t v = stream[o + i];
+    for (uint32_t d = 0; d < J.nfwd; ++d) J.fdst[d][o + i] = v;
+  }
+}
+
+// Relay of one received tile (broadcast): the bytes the tile's flag covers --
+// residual plane(s), directory entries, payload range, the chunk's table and
+// offset on its first tile, header/pads/tail on the last -- are stored as
+// received into the next hops' staging, then their flags are released with
+// the same payload offset.  No decode, no re-encode.
+template <int DT>
+__device__ void forward_tile(const Plan &P, const DecJob &J, uint64_t t, FusedShared &S, uint32_t &fwd_done,
+                             int jidx) {
+  const int tid = threadIdx.x;
+  const StreamGeom &g = J.g;
+  const uint8_t *stream = J.src[0];
+  if (!((fwd_done >> jidx) & 1u)) {  // first forward of this job in this CTA: the hops' slots are free
+    if (tid == 0) {
+      uint32_t ok = 1;
+      for (uint32_t d = 0; d < J.nfwd && ok; ++d) ok = wait_credit(P, J.fcredit[d], J.fepoch[d]);
+      S.abort = ok ? 0u : 1u;
+    }
+    __syncthreads();
+    if (S.abort) return;
+    fwd_done |= 1u << jidx;
+  }
+  const unsigned long long tile_off = S.src_off[0];
+  if (warp_id() == 0) {
+    uint32_t K;
+    unsigned long long off, tile_end;
+    bool bad;
+    tile_block(stream, g, t * kTileBlocks, 0, tile_off, K, off, tile_end, bad);
+    if ((threadIdx.x & 31) == 0) S.ptile_off = bad ? tile_off : tile_end;
+  }
+  __syncthreads();
+  const unsigned long long tile_end = S.ptile_off;
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t nblk = g.n_blocks > b0 ? min((uint64_t)kTileBlocks, g.n_blocks - b0) : 0;
+  if (nblk) {
+    if (DT == kF32) {
+      fwd_range(J, stream, g.off_res0 + 2 * b0 * g.B, 2 * nblk * g.B);
+      fwd_range(J, stream, g.off_res1 + b0 * g.B, nblk * g.B);
+    } else {
+      fwd_range(J, stream, g.off_res0 + b0 * g.B, nblk * g.B);
+    }
+    fwd_range(J, stream, g.off_dir + 4 * b0, 4 * nblk);
+    fwd_range(J, stream, g.off_pay + tile_off, tile_end - tile_off);
+    if (b0 % g.CB == 0) {
+      const uint64_t c = b0 / g.CB;
+      fwd_range(J, stream, g.off_tab + 512 * c, 512);
+      fwd_range(J, stream, g.off_coff + 8 * c, 8);
+    }
+  }
+  if (t == J.ntiles - 1) {  // header, section pads, raw tail
+    fwd_range(J, stream, 0, kHeaderBytes);
+    fwd_range(J, stream, g.off_coff + 8 * g.n_chunks, g.off_dir - (g.off_coff + 8 * g.n_chunks));
+    fwd_range(J, stream, g.off_dir + 4 * g.n_blocks, g.off_pay - (g.off_dir + 4 * g.n_blocks));
+    fwd_range(J, stream, g.off_tail(tile_end), (g.n - g.n_coded) * g.eb);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (uint32_t d = 0; d < J.nfwd; ++d)
+      st_release_sys_u64(J.fflag[d] + t, ((unsigned long long)J.fepoch[d] << 32) | (tile_off >> 4));
+  }
+}
+
 // ---------------------------------------------------------------- D item: decode (+ join)
 template <int DT, int B, bool RED>
 __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &dec_key) {
+                         uint64_t &dec_key, uint32_t &fwd_done) {
   using C = FusedCfg<DT, B>;
   const int tid = threadIdx.x, warp = warp_id();
   const StreamGeom &g = J.g;
@@ -834,6 +910,10 @@ __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, u
     __syncthreads();
     dec_done(J);
     return;
+  }
+  if (J.nfwd) {  // relay first: the next hops receive the tile before it is decoded here
+    forward_tile<DT>(P, J, t, S, fwd_done, jidx);
+    if (S.abort) return;
   }
   uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + P.ring_bytes);
   if (g.n_blocks && need_table) {
@@ -1049,7 +1129,7 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
   __shared__ FusedShared S;
   const int tid = threadIdx.x;
   uint64_t enc_key = ~0ull, dec_key = ~0ull;
-  uint32_t credit_done = 0;
+  uint32_t credit_done = 0, fwd_done = 0;
   using Cf = FusedCfg<DT, B>;
   uint8_t *ring = smem + Cf::kEncTab + kWarps * Cf::kWarpBuf;
   EncPending pd{-1, 0};
@@ -1074,7 +1154,7 @@ __global__ void __launch_bounds__(256, RED ? 1 : 4) k_fused(const __grid_constan
       int j = 0;
       while (j + 1 < P.nd_jobs && k >= P.d[j].ntiles) k -= P.d[j++].ntiles;
       if (RED && P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
-      else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key);
+      else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
     }
     __syncthreads();
     it = uniform_u64(S.tk[par ^ 1]);

@@ -62,6 +62,13 @@ struct DecJob {
   uint32_t epoch[kMaxRanks];
   uint8_t *out;                             // output of this stream / shard
   uint32_t *done;                           // tiles finished (self-resetting counter in ws)
+  // relay (broadcast): every received tile is forwarded, as received, to nfwd peers before it is
+  // decoded; the compressed bytes travel on without re-encoding (weight-sync broadcast)
+  uint32_t nfwd;
+  uint8_t *fdst[kMaxRanks];                 // stream base in each forward destination's staging
+  unsigned long long *fflag[kMaxRanks];     // tile flags there
+  const unsigned long long *fcredit[kMaxRanks];  // local credit words for those slots
+  uint32_t fepoch[kMaxRanks];
 };
 
 struct CopyJob {
@@ -98,6 +105,8 @@ struct EncWs {
     j.tile_status = reinterpret_cast<unsigned long long *>(p);
   }
 };
+
+static_assert(sizeof(Plan) <= 30000, "kernel parameter space");
 
 cudaError_t launch_tables(int dtype, const Plan &p, cudaStream_t st);
 cudaError_t launch_fused(int dtype, const Plan &p, cudaStream_t st, int max_ctas);

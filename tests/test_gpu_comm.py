@@ -260,3 +260,47 @@ def test_mixed_sequence_epochs(uz, orc):
                 assert np.array_equal(host(ys[r], BF16), np.concatenate(a))
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("nr", [2, 3, 4])
+@pytest.mark.parametrize("dtype", [BF16, F32])
+@pytest.mark.parametrize("root", [0, 1])
+def test_broadcast_scatter_relay(uz, orc, nr, dtype, root):
+    """Broadcast (RL weight sync): compressed scatter + relay for >= 3 ranks, fan-out for 2;
+    every rank ends with the root's bytes; multi-round pieces; uneven last piece."""
+    g = Group(uz, nr, **CFG_SMALL)
+    try:
+        n = 3 * (1 << 20) + 4096 * 5 + 13 if dtype == BF16 else (1 << 20) + 4096 + 7
+        bits = gen("W", n, 31 + nr, dtype)
+        bufs = [dev(bits, dtype) if r == root else torch.full((n,), 3, dtype=TD[dtype], device="cuda")
+                for r in range(nr)]
+        for _ in range(2):
+            g.run(lambda r, c, s: c.broadcast(bufs[r], root, s))
+            for r in range(nr):
+                assert np.array_equal(host(bufs[r], dtype), bits), r
+    finally:
+        g.close()
+
+
+def test_broadcast_relay_wire_streams_equal_oracle(uz, orc):
+    """With 3 ranks the root's piece streams, and the relayed copies, are the oracle's streams."""
+    nr, root = 3, 0
+    g = Group(uz, nr, staging_bytes=64 << 20, min_compress_bytes=1)
+    try:
+        n = 4 * (1 << 20) + 40
+        bits = synth.weights(n, 77)
+        bufs = [dev(bits, BF16) if r == root else torch.empty(n, dtype=torch.bfloat16, device="cuda")
+                for r in range(nr)]
+        g.run(lambda r, c, s: c.broadcast(bufs[r], root, s))
+        P = ((n + 1) // 2 + 7) // 8 * 8
+        pieces = [bits[:P], bits[P:]]
+        refs = [orc.compress(BF16, pc) for pc in pieces]
+        # piece 0 -> rank 1 from root; rank 1 relays it to rank 2 (src 1); piece 1 -> rank 2, relayed to rank 1
+        assert g.comms[1].read_staging(root, 0, len(refs[0])) == refs[0]
+        assert g.comms[2].read_staging(root, 0, len(refs[1])) == refs[1]
+        assert g.comms[2].read_staging(1, 0, len(refs[0])) == refs[0]
+        assert g.comms[1].read_staging(2, 0, len(refs[1])) == refs[1]
+        for r in range(nr):
+            assert np.array_equal(host(bufs[r], BF16), bits)
+    finally:
+        g.close()
