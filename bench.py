@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--bytes", type=int, default=1 << 30, help="raw bytes per message (default 1 GiB)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-loopback", action="store_true", help="skip the loopback P2P context field (e.g. under ncu)")
     return ap.parse_args()
 
 
@@ -247,7 +248,7 @@ def run_codec(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_codec_e2e(uz, x, args, stream)
-    loop = run_loopback_p2p(uz, x, args)
+    loop = None if args.no_loopback else run_loopback_p2p(uz, x, args)
 
     line = {
         "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",

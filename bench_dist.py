@@ -128,26 +128,44 @@ def run(args):
     e2e_s = _max_over_ranks(time.perf_counter() - t0) / args.steps
     dist.barrier()
 
-    # allreduce 256 MiB activations (two-shot compressed) vs NCCL
-    T = ((8 if SMOKE else 256) << 20) // (2 * 4096)
+    # collectives on the same box, uzip vs NCCL (algbw = user bytes / time, nccl-tests convention)
+    MB = 1 << 20
+    T = ((8 if SMOKE else 256) * MB) // (2 * 4096)
     ga = torch.Generator(device="cuda")
     ga.manual_seed(3000 + rank)
     scale = torch.exp(torch.randn(4096, device="cuda", generator=ga) * 0.5)
-    a = (torch.randn(T, 4096, device="cuda", generator=ga) * scale).to(torch.bfloat16)
+    a = (torch.randn(T, 4096, device="cuda", generator=ga) * scale).to(torch.bfloat16)  # activations (C4)
     ar_out = torch.empty_like(a)
     nc_buf = a.clone()
+    coll = {}
 
-    def ar_step():
-        with torch.cuda.stream(stream):
-            comm.all_reduce(ar_out, a, stream)
+    def measure(name, uz_fn, nccl_fn, user_bytes):
+        ms_u = _timed(uz_fn, stream, args.steps, args.warmup)
+        stt = comm.stats()
+        ms_n = float("nan") if SMOKE else _timed(nccl_fn, stream, args.steps, args.warmup)
+        coll[name] = {"uzip_algbw_GBps": round(user_bytes / (ms_u / 1e3) / GB, 2),
+                      "nccl_algbw_GBps": round(user_bytes / (ms_n / 1e3) / GB, 2), "ms": round(ms_u, 4),
+                      "ms_nccl": round(ms_n, 4),
+                      "wire_ratio": round(stt["wire_bytes"] / max(1, stt["raw_bytes"]), 5)}
 
-    def ar_nccl():
-        with torch.cuda.stream(stream):
-            dist.all_reduce(nc_buf)
+    def in_stream(f):
+        def g():
+            with torch.cuda.stream(stream):
+                f()
+        return g
 
-    ms_ar = _timed(ar_step, stream, args.steps, args.warmup)
-    ar_stats = comm.stats()
-    ms_ar_nccl = float("nan") if SMOKE else _timed(ar_nccl, stream, args.steps, args.warmup)
+    measure("allreduce_256MiB_act", in_stream(lambda: comm.all_reduce(ar_out, a, stream)),
+            in_stream(lambda: dist.all_reduce(nc_buf)), 2 * a.numel())
+    shard = a.view(-1)[: a.numel() // world]
+    ag_out = torch.empty(world * shard.numel(), dtype=a.dtype, device="cuda")
+    measure("allgather_256MiB_out", in_stream(lambda: comm.all_gather(ag_out, shard, stream)),
+            in_stream(lambda: dist.all_gather_into_tensor(ag_out, shard)), 2 * ag_out.numel())
+    rs_out = torch.empty(a.numel() // world, dtype=a.dtype, device="cuda")
+    measure("reduce_scatter_256MiB_in", in_stream(lambda: comm.reduce_scatter(rs_out, a.view(-1), stream)),
+            in_stream(lambda: dist.reduce_scatter_tensor(rs_out, a.view(-1))), 2 * a.numel())
+    wb = x if rank == 0 else y  # weight-sync broadcast of the 1 GiB W shard from rank 0 (C3 analog)
+    measure("broadcast_1GiB_w", in_stream(lambda: comm.broadcast(wb, 0, stream)),
+            in_stream(lambda: dist.broadcast(wb, 0)), 2 * n)
     assert comm.async_error() == 0
 
     sts = [None] * world
@@ -163,10 +181,7 @@ def run(args):
             "config": bench.config_for(args), "compression_ratio": round(ratio, 5) if ratio else None,
             "nccl_send_recv": {"value": round(raw / (ms_nccl / 1e3) / GB, 3), "unit": "GB/s",
                                "ms_per_step": round(ms_nccl, 4)},
-            "allreduce_256MiB": {"uzip_algbw_GBps": round(2 * a.numel() / (ms_ar / 1e3) / GB, 2),
-                                 "nccl_algbw_GBps": round(2 * a.numel() / (ms_ar_nccl / 1e3) / GB, 2),
-                                 "ms": round(ms_ar, 4), "ms_nccl": round(ms_ar_nccl, 4),
-                                 "wire_ratio": round(ar_stats["wire_bytes"] / max(1, ar_stats["raw_bytes"]), 5)},
+            "collectives": coll,
             "roofline": {"bound": "nvlink", "kernel": "k_fused (sender: encode + P2P stores)",
                          "achieved": round(wire_gbs, 1), "peak": 770.0, "unit": "GB/s",
                          "peak_source": "B200_PROFILING.md measured peer copy per direction",

@@ -170,6 +170,12 @@ UZIP_API uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, s
 UZIP_API uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype,
                              uzip_op_t op, uzip_comm_t comm, void *stream);
 
+/* All-to-all (MoE expert parallelism, KV scatter): sendbuf holds nranks chunks of `count`
+ * elements, chunk j goes to rank j; recvbuf chunk i arrives from rank i.  Each non-own chunk is one
+ * compressed stream (count*eb must be a multiple of 16); the own chunk is copied.  Out of place. */
+UZIP_API uzip_status_t uzip_alltoall(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype,
+                                     uzip_comm_t comm, void *stream);
+
 /* Broadcast (RL weight sync, BASELINE configs[2]): after the call every rank's `buf`
  * holds the root's `count` elements.  Compressed messages (>= the threshold, >= 3 ranks) use a
  * compressed scatter + relay: the root encodes N-1 pieces once and sends piece k to receiver k

@@ -38,6 +38,7 @@ EXPORTED = [
     "uzip_comm_init", "uzip_comm_init_all", "uzip_comm_destroy", "uzip_send", "uzip_recv", "uzip_allgather",
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
     "uzip_status_string", "uzip_version", "uzip_comm_read_staging", "uzip_broadcast",
+    "uzip_alltoall",
 ]
 
 
@@ -104,6 +105,7 @@ def lib() -> ctypes.CDLL:
             l.uzip_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
             l.uzip_comm_read_staging.argtypes = [vp, i32, i32, vp, sz]
             l.uzip_broadcast.argtypes = [vp, sz, i32, i32, vp, vp]
+            l.uzip_alltoall.argtypes = [vp, vp, sz, i32, vp, vp]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
@@ -330,6 +332,12 @@ class Comm:
         inp = out if inp is None else inp
         _check(lib().uzip_allreduce(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), out.numel(),
                                     uz_dtype(out.dtype), SUM, self.h, _stream(stream)), "uzip_allreduce")
+
+    def all_to_all(self, out: torch.Tensor, inp: torch.Tensor, stream=None):
+        """out[i*c:(i+1)*c] <- rank i's inp[me*c:(me+1)*c], c = inp.numel() // nranks."""
+        _check(lib().uzip_alltoall(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                   inp.numel() // self.nranks, uz_dtype(inp.dtype), self.h, _stream(stream)),
+               "uzip_alltoall")
 
     def broadcast(self, t: torch.Tensor, root: int, stream=None):
         _check(lib().uzip_broadcast(ctypes.c_void_p(t.data_ptr()), t.numel(), uz_dtype(t.dtype), root, self.h,

@@ -90,7 +90,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   J.nd = 1;
   J.dst[0] = static_cast<uint8_t *>(out);
   J.d_out_bytes = d_out_bytes;
-  EncWs::carve(w + 64, g.n_chunks, J);
+  EncWs::carve(w + 64, g.n_chunks, g.n_blocks, J);
   p.ne = 1;
   p.n_e_items = J.ntiles;
   cudaStream_t cs = (cudaStream_t)stream;

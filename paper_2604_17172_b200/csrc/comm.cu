@@ -186,7 +186,7 @@ void enc_job(uzip_comm *c, Plan &p, int j, int dt, const uint8_t *in, uint64_t n
   if (compressed) {
     resolve_geom(dt, n, &c->cfg.codec, &J.g);
     J.ntiles = tiles_of(J.g);
-    EncWs::carve(ws_job(c, j), J.g.n_chunks, J);
+    EncWs::carve(ws_job(c, j), J.g.n_chunks, J.g.n_blocks, J);
   } else {
     J.ntiles = std::max<uint64_t>(1, (J.raw_bytes + kRawTileBytes - 1) / kRawTileBytes);
   }
@@ -545,6 +545,52 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
   c->nested = 0;
   c->cfg.min_compress_bytes = saved;
   return s;
+}
+
+uzip_status_t uzip_alltoall(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype, uzip_comm_t c,
+                            void *stream) {
+  if (!valid(c)) return UZIP_ERR_INVALID_ARG;
+  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (count == 0) return UZIP_OK;
+  if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
+  const int dt = (int)dtype;
+  const uint32_t eb = elem_bytes(dt);
+  const int N = c->nranks, me = c->rank;
+  if (N > 1 && (count * eb) % 16 != 0) return UZIP_ERR_INVALID_ARG;  // 16-byte aligned per-peer chunks
+  const uint64_t msg = (uint64_t)N * count * eb;                       // R10: the user message
+  const bool comp = compress_message(c, msg);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (uzip_status_t s = begin_call(c, (uint64_t)(N - 1) * count * eb, comp, st)) return s;
+  const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
+  uint8_t *out = static_cast<uint8_t *>(recvbuf);
+  const uint64_t per = round_elems(c, dt, comp, count, nullptr);
+  const std::vector<int> peers = peers_from(c);
+  for (uint64_t o = 0; o < count; o += per) {
+    const uint64_t n = std::min<uint64_t>(per, count - o);
+    Plan p;
+    base_plan(c, p, dt);
+    int j = 0;
+    for (int d : peers) {  // chunk d of my input -> rank d, one stream each
+      enc_job(c, p, j, dt, in + ((uint64_t)d * count + o) * eb, n, comp, {d});
+      ++j;
+    }
+    j = 0;
+    for (int s : peers) {
+      dec_job(c, p, j, dt, n, comp, {s}, -1, nullptr, out + ((uint64_t)s * count + o) * eb);
+      ++j;
+    }
+    const uint8_t *own = in + ((uint64_t)me * count + o) * eb;
+    uint8_t *own_out = out + ((uint64_t)me * count + o) * eb;
+    if (own != own_out) {
+      p.has_copy = 1;
+      p.c.src = own;
+      p.c.dst = own_out;
+      p.c.bytes = n * eb;
+      p.c.ntiles = (p.c.bytes + kRawTileBytes - 1) / kRawTileBytes;
+    }
+    if (uzip_status_t s = launch(c, p, comp, st)) return s;
+  }
+  return UZIP_OK;
 }
 
 uzip_status_t uzip_broadcast(void *buf, size_t count, uzip_dtype_t dtype, int root, uzip_comm_t c, void *stream) {

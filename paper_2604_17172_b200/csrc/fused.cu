@@ -1,9 +1,10 @@
 // fused.cu -- the Uzip hot path for sm_100a: table build and ONE persistent
 // kernel per launch that encodes, transfers, decodes and reduces.
 //
-//   k_table  a2+a3  sampled per-chunk histogram ("the first 256 KB" of each
-//                   chunk) -> rule-N1 frequencies (R5) -> encode
-//                   reciprocals; one launch covers every stream of a call.
+//   k_hist   a2     sampled per-chunk partial histograms ("the first 256 KB"
+//                   of each chunk), several CTAs per chunk.
+//   k_norm   a3     rule-N1 frequencies (R5) -> encode reciprocals and the
+//                   serialized table; one launch pair covers every stream.
 //   k_fused  E items  a1+a4+a5+a6: split (the residual leaves for every
 //                   destination as soon as it is split: split-send),
 //                   warp-per-block 32-lane rANS,
@@ -29,50 +30,52 @@
 
 namespace uzip {
 
-// ================================================================ k_table
-// grid = (max n_chunks, ne), kTabThreads threads: one CTA per chunk histograms
-// the chunk's sample ("the first 256 KB") with warp-aggregated shared
-// atomics, normalizes (rule N1, R5) and writes the chunk's encode entries and
-// 512-byte serialized table.  No cross-CTA scratch: nothing to reset.
-constexpr int kTabThreads = 512;
-constexpr int kTabWarps = kTabThreads / 32;
+// ================================================================ k_hist + k_norm
+// a2: k_hist, grid (parts, chunks, streams), 256 threads: part p of chunk c
+// histograms its slice of the chunk's sample ("the first 256 KB") with
+// warp-aggregated shared atomics (__match_any_sync) and stores the partial
+// histogram; it also zeroes the look-back words of the k_fused launch that
+// follows.  a3: k_norm, grid (chunks, streams): sums the partials, applies
+// rule N1 (R5) and writes the chunk's encode entries and 512-byte table.
+// Nothing is accumulated across launches, so nothing needs resetting.
+constexpr int kHistThreads = 256;
+constexpr int kHistWarps = kHistThreads / 32;
 
 template <int DT>
-__global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ Plan P) {
-  __shared__ uint32_t hist[kTabWarps][256];
-  __shared__ uint32_t cnt[256];
-  __shared__ unsigned long long red64[8];
-  __shared__ uint32_t red32[8];
-
-  const EncJob &J = P.e[blockIdx.y];
+__global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ Plan P) {
+  __shared__ uint32_t hist[kHistWarps][256];
+  const EncJob &J = P.e[blockIdx.z];
   if (J.raw) return;
   const StreamGeom &g = J.g;
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  const uint32_t c = blockIdx.x;
-
-  // reset the look-back words of this job for the k_fused launch that follows
-  for (uint64_t t = (uint64_t)blockIdx.x * kTabThreads + tid; t < tiles_of(g); t += (uint64_t)gridDim.x * kTabThreads)
-    J.tile_status[t] = 0ull;
+  const uint32_t part = blockIdx.x, c = blockIdx.y;
+  {  // reset the look-back words of this job for the k_fused launch that follows
+    const uint64_t nctas = (uint64_t)gridDim.x * gridDim.y;
+    const uint64_t me = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    for (uint64_t t = me * kHistThreads + tid; t < tiles_of(g); t += nctas * kHistThreads) J.tile_status[t] = 0ull;
+  }
   if (c >= g.n_chunks) return;
-
-  for (int i = tid; i < kTabWarps * 256; i += kTabThreads) (&hist[0][0])[i] = 0;
+  const uint32_t len = g.sample_len(c), parts = hist_parts(len);
+  if (part >= parts) return;
+  for (int i = tid; i < kHistWarps * 256; i += kHistThreads) (&hist[0][0])[i] = 0;
   __syncthreads();
 
-  const uint32_t len = g.sample_len(c);
   constexpr uint32_t kPer = (DT == kF32) ? 4 : 8;  // symbols per 16-byte vector
   constexpr int kUnroll = 8;
   const uint8_t *base = J.in + (uint64_t)c * g.CB * g.B * elem_bytes(DT);
   const uint32_t nvec = len / kPer;
-  for (uint32_t v0 = 0; v0 < nvec; v0 += kTabThreads * kUnroll) {
+  const uint32_t per = (nvec + parts - 1) / parts;
+  const uint32_t v_lo = part * per, v_hi = min(nvec, v_lo + per);
+  for (uint32_t v0 = v_lo; v0 < v_hi; v0 += kHistThreads * kUnroll) {
     uint4 w[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const uint32_t v = v0 + u * kTabThreads + tid;
-      w[u] = v < nvec ? ldg_nc_v4(base + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+      const uint32_t v = v0 + u * kHistThreads + tid;
+      w[u] = v < v_hi ? ldg_nc_v4(base + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const bool ok = v0 + u * kTabThreads + tid < nvec;
+      const bool ok = v0 + u * kHistThreads + tid < v_hi;
       uint32_t s_lo, s_hi = 0;
       if (DT == kBF16) {
         uint32_t r;
@@ -90,31 +93,44 @@ __global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ P
       // warp-aggregated increments: the lanes holding the same symbol add once
 #pragma unroll
       for (int k = 0; k < (int)kPer; ++k) {
-        const uint32_t s = ok ? ((k < 4 ? s_lo : s_hi) >> (8 * (k & 3))) & 0xFFu : 0x100u;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, s);
-        if (s < 256 && (uint32_t)lane == (uint32_t)(__ffs(peers) - 1))
-          atomicAdd(&hist[warp][s], (uint32_t)__popc(peers));
+        const uint32_t sy = ok ? ((k < 4 ? s_lo : s_hi) >> (8 * (k & 3))) & 0xFFu : 0x100u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, sy);
+        if (sy < 256 && (uint32_t)lane == (uint32_t)(__ffs(peers) - 1))
+          atomicAdd(&hist[warp][sy], (uint32_t)__popc(peers));
       }
     }
   }
-  for (uint32_t i = nvec * kPer + tid; i < len; i += kTabThreads) {  // sample length not a vector multiple
-    uint32_t s;
-    if (DT == kF32) s = (reinterpret_cast<const uint32_t *>(base)[i] >> 23) & 0xFFu;
-    else if (DT == kBF16) s = (reinterpret_cast<const uint16_t *>(base)[i] >> 7) & 0xFFu;
-    else s = reinterpret_cast<const uint16_t *>(base)[i] >> 8;
-    atomicAdd(&hist[warp][s], 1u);
-  }
+  if (part == parts - 1)
+    for (uint32_t i = nvec * kPer + tid; i < len; i += kHistThreads) {  // sample not a vector multiple
+      uint32_t sy;
+      if (DT == kF32) sy = (reinterpret_cast<const uint32_t *>(base)[i] >> 23) & 0xFFu;
+      else if (DT == kBF16) sy = (reinterpret_cast<const uint16_t *>(base)[i] >> 7) & 0xFFu;
+      else sy = reinterpret_cast<const uint16_t *>(base)[i] >> 8;
+      atomicAdd(&hist[warp][sy], 1u);
+    }
   __syncthreads();
-  if (tid >= 256) return;  // 8 warps normalize
-
-  // ---- rule N1 (R5)
-  {
-    uint32_t sum = 0;
+  uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < kTabWarps; ++w) sum += hist[w][tid];
-    cnt[tid] = sum;
-  }
-  // total and argmax (lowest symbol on ties): key = cnt<<8 | (255 - s)
+  for (int w = 0; w < kHistWarps; ++w) sum += hist[w][tid];
+  J.partial[((uint64_t)c * kMaxHistParts + part) * 256 + tid] = sum;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
+  __shared__ uint32_t cnt[256];
+  __shared__ unsigned long long red64[8];
+  __shared__ uint32_t red32[8];
+  const EncJob &J = P.e[blockIdx.y];
+  if (J.raw) return;
+  const StreamGeom &g = J.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const uint32_t c = blockIdx.x;
+  if (c >= g.n_chunks) return;
+  const uint32_t parts = hist_parts(g.sample_len(c));
+  uint32_t sum = 0;
+  for (uint32_t p = 0; p < parts; ++p) sum += J.partial[((uint64_t)c * kMaxHistParts + p) * 256 + tid];
+  cnt[tid] = sum;
+  // ---- rule N1 (R5): total and argmax (lowest symbol on ties): key = cnt<<8 | (255 - s)
   unsigned long long key = ((unsigned long long)cnt[tid] << 8) | (255u - tid);
   unsigned long long tot = cnt[tid];
   for (int o = 16; o; o >>= 1) {
@@ -126,7 +142,7 @@ __global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ P
     red64[warp] = key;
     red32[warp] = (uint32_t)tot;
   }
-  asm volatile("bar.sync 1, 256;");
+  __syncthreads();
   unsigned long long best_key = 0, total = 0;
   for (int w = 0; w < 8; ++w) {
     best_key = red64[w] > best_key ? red64[w] : best_key;
@@ -136,22 +152,22 @@ __global__ void __launch_bounds__(kTabThreads) k_table(const __grid_constant__ P
   uint32_t f;
   if (total == 0) f = kM / 256;
   else f = 1u + (uint32_t)(((unsigned long long)cnt[tid] * (kM - 256)) / total);
-  asm volatile("bar.sync 1, 256;");
+  __syncthreads();
   uint32_t fs = f;
   for (int o = 16; o; o >>= 1) fs += __shfl_xor_sync(0xFFFFFFFFu, fs, o);
   if (lane == 0) red32[warp] = fs;
-  asm volatile("bar.sync 1, 256;");
+  __syncthreads();
   uint32_t fsum = 0;
   for (int w = 0; w < 8; ++w) fsum += red32[w];
   if (total != 0 && tid == (int)best) f += kM - fsum;
-  asm volatile("bar.sync 1, 256;");
+  __syncthreads();
   uint32_t incl = f;  // exclusive prefix (cdf) over 256 symbols
   for (int o = 1; o < 32; o <<= 1) {
     uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
     if (lane >= o) incl += t;
   }
   if (lane == 31) red32[warp] = incl;
-  asm volatile("bar.sync 1, 256;");
+  __syncthreads();
   uint32_t woff = 0;
   for (int w = 0; w < warp; ++w) woff += red32[w];
   const uint32_t cdf = woff + incl - f;
@@ -389,6 +405,10 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
   // ND1: one destination (codec, P2P): the residual bases are computed once
   uint8_t *r0 = J.dst[0] + g.off_res0 + (DT == kF32 ? 2 : 1) * (b * B);
   uint8_t *r1 = J.dst[0] + g.off_res1 + b * B;
+  // byte of the lane's first vector in buf; later vectors of the lane step by kVec*32 elements (one row
+  // group), backwards in coding order (REV) -- an immediate offset in the store
+  const uint32_t e0 = (uint32_t)lane * C::kVec;
+  uint8_t *pos0 = buf + (REV ? (uint32_t)(B - 32) - (e0 & ~31u) + (e0 & 31u) : e0);
 #pragma unroll
   for (int h = 0; h < C::kIters; h += C::kBatch) {
     uint4 v[C::kBatch];
@@ -396,13 +416,13 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
     for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
 #pragma unroll
     for (int i = 0; i < C::kBatch; ++i) {
-      const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;            // element within block
-      const uint32_t pos = REV ? (uint32_t)(B - 32) - (e & ~31u) + (e & 31u) : e;  // byte in buf
+      const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;  // element within block
+      uint8_t *sp = REV ? pos0 - 32 * C::kVec * (h + i) : pos0 + 32 * C::kVec * (h + i);
       if (DT == kF32) {
         uint32_t s4, h4;
         uint2 lo;
         split4_f32(v[i], s4, lo, h4);
-        *reinterpret_cast<uint32_t *>(buf + pos) = s4;
+        *reinterpret_cast<uint32_t *>(sp) = s4;
         if (RES) {
           if (ND1) {
             *reinterpret_cast<uint2 *>(r0 + 2 * e) = lo;
@@ -423,7 +443,7 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
           split4_f16(v[i].x, v[i].y, s0, q0);
           split4_f16(v[i].z, v[i].w, s1, q1);
         }
-        *reinterpret_cast<uint2 *>(buf + pos) = make_uint2(s0, s1);
+        *reinterpret_cast<uint2 *>(sp) = make_uint2(s0, s1);
         if (RES) {
           if (ND1) {
             *reinterpret_cast<uint2 *>(r0 + e) = make_uint2(q0, q1);
@@ -1186,10 +1206,18 @@ int sm_count() {
 template <int DT>
 cudaError_t launch_tables_t(const Plan &p, cudaStream_t st) {
   uint64_t max_chunks = 1;  // >= 1: the look-back words are reset even without chunks
-  for (int j = 0; j < p.ne; ++j)
-    if (!p.e[j].raw) max_chunks = p.e[j].g.n_chunks > max_chunks ? p.e[j].g.n_chunks : max_chunks;
-  dim3 grid((unsigned)max_chunks, (unsigned)p.ne);
-  k_table<DT><<<grid, kTabThreads, 0, st>>>(p);
+  uint32_t max_parts = 1;
+  for (int j = 0; j < p.ne; ++j) {
+    const EncJob &J = p.e[j];
+    if (J.raw) continue;
+    max_chunks = J.g.n_chunks > max_chunks ? J.g.n_chunks : max_chunks;
+    for (uint64_t c = 0; c < J.g.n_chunks; c += (J.g.n_chunks > 1 ? J.g.n_chunks - 1 : 1)) {
+      const uint32_t parts = hist_parts(J.g.sample_len(c));
+      max_parts = parts > max_parts ? parts : max_parts;
+    }
+  }
+  k_hist<DT><<<dim3(max_parts, (unsigned)max_chunks, (unsigned)p.ne), kHistThreads, 0, st>>>(p);
+  k_norm<DT><<<dim3((unsigned)max_chunks, (unsigned)p.ne), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -43,7 +43,8 @@ struct EncJob {
   uint32_t epoch[kMaxRanks];                // flag epoch per destination (round sequence + 1)
   uint4 *enc;                               // per-chunk encode entries (k_table)
   uint16_t *tab16;                          // per-chunk serialized tables (k_table)
-  unsigned long long *tile_status;          // per-block look-back words (zeroed by k_table)
+  unsigned long long *tile_status;          // per-tile look-back words (zeroed by k_hist)
+  uint32_t *partial;                        // k_hist partial histograms [chunk][kMaxHistParts][256]
   uint64_t *d_out_bytes;                    // codec: stream size (may be null)
   unsigned long long *wire_acc;             // comm: += stream bytes x nd (may be null)
 };
@@ -90,19 +91,29 @@ struct Plan {
   int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
 };
 
+// k_hist splits a chunk's sample over up to kMaxHistParts CTAs of >= 16 Ki symbols.
+constexpr uint32_t kMaxHistParts = 64;
+__host__ __device__ inline uint32_t hist_parts(uint32_t sample_len) {
+  const uint32_t p = (sample_len + 16383) / 16384;
+  return p < 1 ? 1 : (p > kMaxHistParts ? kMaxHistParts : p);
+}
+
 // Workspace of one encode job: enc entries, serialized tables, look-back
-// words (all written by k_table before use: no state survives a launch, so
-// the layout may change from call to call).
+// words, partial histograms (all written by k_hist/k_norm before use: no state
+// survives a launch, so the layout may change from call to call).
 struct EncWs {
   static uint64_t bytes(uint64_t n_chunks, uint64_t n_blocks) {
-    return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * (n_blocks + 1));
+    return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * (n_blocks + 1)) +
+           round16(1024ull * kMaxHistParts * n_chunks);
   }
-  static void carve(uint8_t *p, uint64_t n_chunks, EncJob &j) {
+  static void carve(uint8_t *p, uint64_t n_chunks, uint64_t n_blocks, EncJob &j) {
     j.enc = reinterpret_cast<uint4 *>(p);
     p += round16(4096 * n_chunks);
     j.tab16 = reinterpret_cast<uint16_t *>(p);
     p += round16(512 * n_chunks);
     j.tile_status = reinterpret_cast<unsigned long long *>(p);
+    p += round16(8 * (n_blocks + 1));
+    j.partial = reinterpret_cast<uint32_t *>(p);
   }
 };
 

@@ -224,6 +224,13 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return r;
 }
 
+// (m & a) | (~m & b) as one LOP3
+__device__ __forceinline__ uint32_t bitselect(uint32_t m, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(r) : "r"(m), "r"(a), "r"(b));
+  return r;
+}
+
 // ---------------------------------------------------------------- a1 split / join
 // Split of one 16-byte vector into symbols and residual (DESIGN.md
 // section 2).  Byte-permute forms: 1.5 ALU ops per element.
@@ -232,7 +239,7 @@ __device__ __forceinline__ void split4_bf16(uint32_t w0, uint32_t w1, uint32_t &
   sym4 = __byte_perm(w0 >> 7, w1 >> 7, 0x6420);
   uint32_t lo = __byte_perm(w0, w1, 0x6420);
   uint32_t hi = __byte_perm(w0, w1, 0x7531);
-  res4 = (lo & 0x7F7F7F7Fu) | (hi & 0x80808080u);
+  res4 = bitselect(0x80808080u, hi, lo);  // (hi & 0x80..) | (lo & 0x7F..) in one LOP3
 }
 // f16: symbol = high byte, residual = low byte (R3).
 __device__ __forceinline__ void split4_f16(uint32_t w0, uint32_t w1, uint32_t &sym4, uint32_t &res4) {

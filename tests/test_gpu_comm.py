@@ -304,3 +304,22 @@ def test_broadcast_relay_wire_streams_equal_oracle(uz, orc):
             assert np.array_equal(host(bufs[r], BF16), bits)
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("nr", [2, 3, 4])
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+def test_alltoall(uz, nr, dtype):
+    """All-to-all: out_r[i] == in_i[r] for every pair, compressed per-peer streams."""
+    g = Group(uz, nr, **CFG_SMALL)
+    try:
+        c = (1 << 20) + 4096 + 8
+        ins = [gen("W", nr * c, 600 + r, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(nr * c, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        for _ in range(2):
+            g.run(lambda r, cm, s: cm.all_to_all(outs[r], xs[r], s))
+            for r in range(nr):
+                ref = np.concatenate([ins[i][r * c:(r + 1) * c] for i in range(nr)])
+                assert np.array_equal(host(outs[r], dtype), ref), r
+    finally:
+        g.close()
