@@ -301,12 +301,14 @@ def run_loopback_p2p(uz, x, args):
     e1.record(s0)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    ok = torch.equal(x.view(torch.int16), y.view(torch.int16)) and comms[0].async_error() == 0
+    errs = [c.async_error() for c in comms]
+    ok = torch.equal(x.view(torch.int16), y.view(torch.int16)) and errs == [0, 0]
     st = comms[0].stats()
     for c in comms:
         c.destroy()
     return {"value": round(x.numel() * 2 / (ms / 1e3) / GB, 2), "unit": "GB/s", "ms": round(ms, 4),
-            "bit_exact": bool(ok), "wire_ratio": round(st["wire_bytes"] / max(1, st["raw_bytes"]), 5),
+            "bit_exact": bool(ok), "async_errors": errs,
+            "wire_ratio": round(st["wire_bytes"] / max(1, st["raw_bytes"]), 5),
             "note": "sender+receiver kernels share one GPU (loopback), 1 GiB bf16 W"}
 
 

@@ -71,6 +71,7 @@ def run(args):
     x = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     y = torch.empty_like(x)
     pairs = world // 2
+    raw = pairs * 2 * n
     role = "send" if rank % 2 == 0 and rank + 1 < world else ("recv" if rank % 2 == 1 else "idle")
     peer = rank + 1 if role == "send" else rank - 1
 
@@ -100,6 +101,39 @@ def run(args):
         dist.recv(ref, peer)
         assert torch.equal(ref.view(torch.int16).cpu(), y.view(torch.int16).cpu()), "P2P mismatch"
     ms_nccl = float("nan") if SMOKE else _timed(nccl_step, stream, args.steps, args.warmup)
+
+    # ablation (fig:compare_with_native_pipeline): encode-send = compress the whole
+    # message, ship the stream with NCCL, decompress -- no overlap, no fused transfer
+    ablation = {}
+    if not SMOKE:
+        cap = uz.compress_bound(n, uz.BF16)
+        sbuf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+        stat = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ws = uz.Workspace(local).get(uz.workspace_bytes(n, uz.BF16), stream)
+        with torch.cuda.stream(stream):
+            if role == "send":
+                uz.compress(x, out=sbuf, out_bytes=nb, stream=stream, ws=ws)
+        torch.cuda.synchronize()
+        szt = nb.clone()
+        if role == "send":
+            dist.send(szt, peer)  # the stream size is deterministic for this input: exchanged once
+        elif role == "recv":
+            dist.recv(szt, peer)
+        wire = int(szt.item())
+
+        def encode_send():
+            with torch.cuda.stream(stream):
+                if role == "send":
+                    uz.compress(x, out=sbuf, out_bytes=nb, stream=stream, ws=ws)
+                    dist.send(sbuf[:wire], peer)
+                elif role == "recv":
+                    dist.recv(sbuf[:wire], peer)
+                    uz.decompress(sbuf, n, uz.BF16, out=y, status=stat, stream=stream, ws=ws, in_bytes=wire)
+
+        ms_es = _timed(encode_send, stream, args.steps, args.warmup)
+        ablation = {"encode_send_GBps": round(raw / (ms_es / 1e3) / GB, 3), "ms": round(ms_es, 4),
+                    "note": "uzip_compress + NCCL send of the stream + uzip_decompress, serial"}
 
     # e2e through the public API with host buffers: the sender copies its input from pinned host memory
     # and sends; the receiver receives and reads 16 bytes of the result back; wall clock, max over ranks
@@ -171,7 +205,6 @@ def run(args):
     sts = [None] * world
     dist.all_gather_object(sts, st)
     if rank == 0:
-        raw = pairs * 2 * n
         ratio = next((s["wire_bytes"] / s["raw_bytes"] for s in sts if s), None)
         wire_gbs = (ratio or 1.0) * 2 * n / (ms / 1e3) / GB
         line = {
@@ -182,6 +215,7 @@ def run(args):
             "nccl_send_recv": {"value": round(raw / (ms_nccl / 1e3) / GB, 3), "unit": "GB/s",
                                "ms_per_step": round(ms_nccl, 4)},
             "collectives": coll,
+            "ablation": ablation,
             "roofline": {"bound": "nvlink", "kernel": "k_fused (sender: encode + P2P stores)",
                          "achieved": round(wire_gbs, 1), "peak": 770.0, "unit": "GB/s",
                          "peak_source": "B200_PROFILING.md measured peer copy per direction",

@@ -200,6 +200,13 @@ typedef struct uzip_stats {
 } uzip_stats_t;
 UZIP_API uzip_status_t uzip_get_stats(uzip_comm_t comm, uzip_stats_t *out);
 
+/* Debug: the async error word and where the first error happened (sync read into 16 words):
+ * [0] status, [1] site (1 tile flag, 2 credit, 3 look-back), [2] expected epoch / tile,
+ * [3..4] value seen (hi, lo), [5] low 32 bits of the polled address, [6] CTA index,
+ * [7] rounds sent | received << 16 on the channel with the first other rank, [8..11] this rank's
+ * credit words for peers 0 and 1 (slots 0, 1), [12..15] decode-job done counters 0..3. */
+UZIP_API uzip_status_t uzip_comm_error_detail(uzip_comm_t comm, uint32_t *out16);
+
 /* Debug/test: copy the first `bytes` of the staging slot (0 or 1) where
  * rank `src`'s rounds land on this rank into host memory (sync).  Round q of
  * the ordered pair (src, this rank) lands in slot q % 2 as one UZB1 stream

@@ -20,7 +20,7 @@ import torch
 from . import _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libuzip.so")
+LIB_PATH = os.environ.get("UZIP_LIB_PATH") or os.path.join(_HERE, "libuzip.so")  # override: tuning variants
 
 BF16, F16, F32 = 0, 1, 2
 SUM = 0
@@ -38,7 +38,7 @@ EXPORTED = [
     "uzip_comm_init", "uzip_comm_init_all", "uzip_comm_destroy", "uzip_send", "uzip_recv", "uzip_allgather",
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
     "uzip_status_string", "uzip_version", "uzip_comm_read_staging", "uzip_broadcast",
-    "uzip_alltoall",
+    "uzip_alltoall", "uzip_comm_error_detail",
 ]
 
 
@@ -106,6 +106,7 @@ def lib() -> ctypes.CDLL:
             l.uzip_comm_read_staging.argtypes = [vp, i32, i32, vp, sz]
             l.uzip_broadcast.argtypes = [vp, sz, i32, i32, vp, vp]
             l.uzip_alltoall.argtypes = [vp, vp, sz, i32, vp, vp]
+            l.uzip_comm_error_detail.argtypes = [vp, vp]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
@@ -347,6 +348,11 @@ class Comm:
         e = ctypes.c_int(0)
         _check(lib().uzip_comm_get_async_error(self.h, ctypes.byref(e)), "uzip_comm_get_async_error")
         return e.value
+
+    def error_detail(self) -> list:
+        buf = (ctypes.c_uint32 * 16)()
+        _check(lib().uzip_comm_error_detail(self.h, buf), "uzip_comm_error_detail")
+        return list(buf)
 
     def stats(self) -> dict:
         s = Stats()

@@ -32,17 +32,20 @@ def _stale() -> bool:
     return max(os.path.getmtime(p) for p in deps) > os.path.getmtime(LIB)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libuzip.so (or a variant at `out` with extra -D defines, for tuning experiments)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
     for src in sources():  # one nvcc per translation unit, in parallel
         obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
         objs.append(obj)
-        cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", obj, src]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *(["-Xptxas", "-v"] if verbose else []), "-c", "-o",
+               obj, src]
         procs.append((subprocess.Popen(cmd), cmd))
     for p, cmd in procs:
         if p.wait() != 0:
@@ -50,8 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
     for o in objs:
         os.remove(o)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -107,6 +107,7 @@ uzip_status_t alloc_local(uzip_comm *c) {
   if (cudaMalloc(&c->ws, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaMemset(c->ws, 0, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return UZIP_ERR_CUDA;
+  if (preload_kernels() != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaDeviceSynchronize() != cudaSuccess) return UZIP_ERR_CUDA;
   return UZIP_OK;
 }
@@ -674,6 +675,21 @@ uzip_status_t uzip_comm_get_async_error(uzip_comm_t c, uzip_status_t *err) {
   if (cudaStreamSynchronize(c->side) != cudaSuccess) return UZIP_ERR_CUDA;
   *err = (uzip_status_t)v;
   return UZIP_OK;
+}
+
+uzip_status_t uzip_comm_error_detail(uzip_comm_t c, uint32_t *out16) {
+  if (!valid(c) || !out16) return UZIP_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  unsigned long long cr[4] = {0, 0, 0, 0};
+  bool ok = cudaMemcpyAsync(out16, c->region, 32, cudaMemcpyDeviceToHost, c->side) == cudaSuccess;
+  for (int d = 0; d < 2 && d < c->nranks; ++d)  // credit words of peers 0,1 (slots 0,1)
+    ok &= cudaMemcpyAsync(cr + 2 * d, c->region + c->L.credit(d, 0), 16, cudaMemcpyDeviceToHost, c->side) ==
+          cudaSuccess;
+  ok &= cudaMemcpyAsync(out16 + 12, c->ws + 16, 16, cudaMemcpyDeviceToHost, c->side) == cudaSuccess;
+  ok &= cudaStreamSynchronize(c->side) == cudaSuccess;
+  for (int i = 0; i < 4; ++i) out16[8 + i] = (uint32_t)cr[i];
+  out16[7] = c->send_seq[c->rank ? 0 : 1] | (c->recv_seq[c->rank ? 0 : 1] << 16);
+  return ok ? UZIP_OK : UZIP_ERR_CUDA;
 }
 
 uzip_status_t uzip_comm_read_staging(uzip_comm_t c, int src, int slot, void *host, size_t bytes) {

@@ -1,0 +1,10 @@
+// fused_f16_enc.cu -- instantiates the fused kernels for f16, encode/decode variant.
+#include "fused_impl.cuh"
+
+namespace uzip {
+cudaError_t launch_tables_f16(const Plan &p, cudaStream_t st) { return launch_tables_t<kF16>(p, st); }
+cudaError_t launch_fused_f16_enc(const Plan &p, uint32_t B, cudaStream_t st, int max_ctas) {
+  return launch_fused_b<kF16, false>(p, B, st, max_ctas);
+}
+cudaError_t preload_f16_enc() { return preload_t<kF16, false>(); }
+}  // namespace uzip

@@ -1,0 +1,9 @@
+// fused_f16_red.cu -- instantiates the fused kernels for f16, reduce variant.
+#include "fused_impl.cuh"
+
+namespace uzip {
+cudaError_t launch_fused_f16_red(const Plan &p, uint32_t B, cudaStream_t st, int max_ctas) {
+  return launch_fused_b<kF16, true>(p, B, st, max_ctas);
+}
+cudaError_t preload_f16_red() { return preload_t<kF16, true>(); }
+}  // namespace uzip

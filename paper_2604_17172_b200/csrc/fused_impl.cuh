@@ -1,0 +1,1321 @@
+// fused_impl.cuh -- the Uzip hot path for sm_100a (templates; instantiated per
+// dtype and variant in fused_<dtype>_<enc|red>.cu so nvcc runs in parallel): table build and ONE persistent
+// kernel per launch that encodes, transfers, decodes and reduces.
+//
+//   k_hist   a2     sampled per-chunk partial histograms ("the first 256 KB"
+//                   of each chunk), several CTAs per chunk.
+//   k_norm   a3     rule-N1 frequencies (R5) -> encode reciprocals and the
+//                   serialized table; one launch pair covers every stream.
+//   k_fused  E items  a1+a4+a5+a6: split (the residual leaves for every
+//                   destination as soon as it is split: split-send),
+//                   warp-per-block 32-lane rANS,
+//                   decoupled look-back so each block is stored once at its
+//                   final offset (Step 3 removed), stores straight
+//                   into the destinations' staging, tile flag
+//                   release (a12).
+//            C items  plain copies (own allgather shard).
+//            D items  a7+a8(+a9): acquire a tile flag, decode (table-driven),
+//                   join; with several sources, decode each and fold in rank
+//                   order in fp32 before one rounding (R11).
+//
+// Stream bytes equal the CPU oracle's (tests/test_gpu_codec.py,
+// tests/test_gpu_comm.py); layout in DESIGN.md section 2.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdio>
+
+#include "codec_dev.cuh"
+#include "plan.h"
+#include "uzip_internal.h"
+
+// Tuning knobs (defaults measured best on B200; overridable for experiments with -D)
+#ifndef UZIP_ENC_GROUP
+#define UZIP_ENC_GROUP 8  // encoder rounds whose symbols/table entries are loaded ahead
+#endif
+#ifndef UZIP_ENC_MINB
+#define UZIP_ENC_MINB 3   // resident CTAs per SM targeted by launches with encode items (measured)
+#endif
+
+namespace uzip {
+
+// ================================================================ k_hist + k_norm
+// a2: k_hist, grid (parts, chunks, streams), 256 threads: part p of chunk c
+// histograms its slice of the chunk's sample ("the first 256 KB") with
+// warp-aggregated shared atomics (__match_any_sync) and stores the partial
+// histogram; it also zeroes the look-back words of the k_fused launch that
+// follows.  a3: k_norm, grid (chunks, streams): sums the partials, applies
+// rule N1 (R5) and writes the chunk's encode entries and 512-byte table.
+// Nothing is accumulated across launches, so nothing needs resetting.
+constexpr int kHistThreads = 256;
+constexpr int kHistWarps = kHistThreads / 32;
+
+template <int DT>
+__global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ Plan P) {
+  __shared__ uint32_t hist[kHistWarps][256];
+  const EncJob &J = P.e[blockIdx.z];
+  if (J.raw) return;
+  const StreamGeom &g = J.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const uint32_t part = blockIdx.x, c = blockIdx.y;
+  {  // reset the look-back words of this job for the k_fused launch that follows
+    const uint64_t nctas = (uint64_t)gridDim.x * gridDim.y;
+    const uint64_t me = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    for (uint64_t t = me * kHistThreads + tid; t < tiles_of(g); t += nctas * kHistThreads) J.tile_status[t] = 0ull;
+  }
+  if (c >= g.n_chunks) return;
+  const uint32_t len = g.sample_len(c), parts = hist_parts(len);
+  if (part >= parts) return;
+  for (int i = tid; i < kHistWarps * 256; i += kHistThreads) (&hist[0][0])[i] = 0;
+  __syncthreads();
+
+  constexpr uint32_t kPer = (DT == kF32) ? 4 : 8;  // symbols per 16-byte vector
+  constexpr int kUnroll = 8;
+  const uint8_t *base = J.in + (uint64_t)c * g.CB * g.B * elem_bytes(DT);
+  const uint32_t nvec = len / kPer;
+  const uint32_t per = (nvec + parts - 1) / parts;
+  const uint32_t v_lo = part * per, v_hi = min(nvec, v_lo + per);
+  for (uint32_t v0 = v_lo; v0 < v_hi; v0 += kHistThreads * kUnroll) {
+    uint4 w[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t v = v0 + u * kHistThreads + tid;
+      w[u] = v < v_hi ? ldg_nc_v4(base + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const bool ok = v0 + u * kHistThreads + tid < v_hi;
+      uint32_t s_lo, s_hi = 0;
+      if (DT == kBF16) {
+        uint32_t r;
+        split4_bf16(w[u].x, w[u].y, s_lo, r);
+        split4_bf16(w[u].z, w[u].w, s_hi, r);
+      } else if (DT == kF16) {
+        uint32_t r;
+        split4_f16(w[u].x, w[u].y, s_lo, r);
+        split4_f16(w[u].z, w[u].w, s_hi, r);
+      } else {
+        uint2 lo;
+        uint32_t hi;
+        split4_f32(w[u], s_lo, lo, hi);
+      }
+      // warp-aggregated increments: the lanes holding the same symbol add once
+#pragma unroll
+      for (int k = 0; k < (int)kPer; ++k) {
+        const uint32_t sy = ok ? ((k < 4 ? s_lo : s_hi) >> (8 * (k & 3))) & 0xFFu : 0x100u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, sy);
+        if (sy < 256 && (uint32_t)lane == (uint32_t)(__ffs(peers) - 1))
+          atomicAdd(&hist[warp][sy], (uint32_t)__popc(peers));
+      }
+    }
+  }
+  if (part == parts - 1)
+    for (uint32_t i = nvec * kPer + tid; i < len; i += kHistThreads) {  // sample not a vector multiple
+      uint32_t sy;
+      if (DT == kF32) sy = (reinterpret_cast<const uint32_t *>(base)[i] >> 23) & 0xFFu;
+      else if (DT == kBF16) sy = (reinterpret_cast<const uint16_t *>(base)[i] >> 7) & 0xFFu;
+      else sy = reinterpret_cast<const uint16_t *>(base)[i] >> 8;
+      atomicAdd(&hist[warp][sy], 1u);
+    }
+  __syncthreads();
+  uint32_t sum = 0;
+#pragma unroll
+  for (int w = 0; w < kHistWarps; ++w) sum += hist[w][tid];
+  J.partial[((uint64_t)c * kMaxHistParts + part) * 256 + tid] = sum;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
+  __shared__ uint32_t cnt[256];
+  __shared__ unsigned long long red64[8];
+  __shared__ uint32_t red32[8];
+  const EncJob &J = P.e[blockIdx.y];
+  if (J.raw) return;
+  const StreamGeom &g = J.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const uint32_t c = blockIdx.x;
+  if (c >= g.n_chunks) return;
+  const uint32_t parts = hist_parts(g.sample_len(c));
+  uint32_t sum = 0;
+  for (uint32_t p = 0; p < parts; ++p) sum += J.partial[((uint64_t)c * kMaxHistParts + p) * 256 + tid];
+  cnt[tid] = sum;
+  // ---- rule N1 (R5): total and argmax (lowest symbol on ties): key = cnt<<8 | (255 - s)
+  unsigned long long key = ((unsigned long long)cnt[tid] << 8) | (255u - tid);
+  unsigned long long tot = cnt[tid];
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long ok = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+    key = ok > key ? ok : key;
+    tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+  }
+  if (lane == 0) {
+    red64[warp] = key;
+    red32[warp] = (uint32_t)tot;
+  }
+  __syncthreads();
+  unsigned long long best_key = 0, total = 0;
+  for (int w = 0; w < 8; ++w) {
+    best_key = red64[w] > best_key ? red64[w] : best_key;
+    total += red32[w];
+  }
+  const uint32_t best = 255u - (uint32_t)(best_key & 0xFFu);
+  uint32_t f;
+  if (total == 0) f = kM / 256;
+  else f = 1u + (uint32_t)(((unsigned long long)cnt[tid] * (kM - 256)) / total);
+  __syncthreads();
+  uint32_t fs = f;
+  for (int o = 16; o; o >>= 1) fs += __shfl_xor_sync(0xFFFFFFFFu, fs, o);
+  if (lane == 0) red32[warp] = fs;
+  __syncthreads();
+  uint32_t fsum = 0;
+  for (int w = 0; w < 8; ++w) fsum += red32[w];
+  if (total != 0 && tid == (int)best) f += kM - fsum;
+  __syncthreads();
+  uint32_t incl = f;  // exclusive prefix (cdf) over 256 symbols
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) red32[warp] = incl;
+  __syncthreads();
+  uint32_t woff = 0;
+  for (int w = 0; w < warp; ++w) woff += red32[w];
+  const uint32_t cdf = woff + incl - f;
+  J.enc[c * 256 + tid] = make_enc_entry(f, cdf);
+  J.tab16[c * 256 + tid] = (uint16_t)f;
+}
+
+// ================================================================ shared pieces
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagInc = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void raise_err(const Plan &P, uint32_t code) { atomicCAS(P.err, 0u, code); }
+// First error only: the code plus where it happened (site, expected, seen) for uzip_comm_error_detail.
+__device__ __forceinline__ void raise_err_at(const Plan &P, uint32_t code, uint32_t site, uint32_t expect,
+                                             unsigned long long seen, uint64_t where) {
+  if (atomicCAS(P.err, 0u, code) == 0u) {
+    P.err[1] = site;
+    P.err[2] = expect;
+    P.err[3] = (uint32_t)(seen >> 32);
+    P.err[4] = (uint32_t)seen;
+    P.err[5] = (uint32_t)where;
+    P.err[6] = blockIdx.x;
+    __threadfence_system();
+  }
+}
+
+// Poll a tile flag until its epoch matches (thread-level; bounded by the
+// plan's timeout, aborts when another CTA raised an error).
+static __device__ bool wait_flag(const Plan &P, const unsigned long long *f, uint32_t epoch, unsigned long long &v) {
+  unsigned long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    v = ld_acquire_sys_u64(f);
+    if ((uint32_t)(v >> 32) == epoch) return true;
+    if ((spin & 63) == 63) {
+      if (ld_volatile_u32(P.err)) return false;
+      const unsigned long long now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > P.timeout_ns) {
+        raise_err_at(P, UZIP_ERR_TIMEOUT, 1, epoch, v, (uint64_t)(uintptr_t)f);
+        return false;
+      }
+    }
+    __nanosleep(32);
+  }
+}
+
+// Credit: the destination consumed epoch-2 from this slot (a12).
+static __device__ bool wait_credit(const Plan &P, const unsigned long long *cr, uint32_t epoch) {
+  if (!cr || epoch <= 2) return true;
+  unsigned long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    if (ld_acquire_sys_u64(cr) >= (unsigned long long)(epoch - 2)) return true;
+    if ((spin & 63) == 63) {
+      if (ld_volatile_u32(P.err)) return false;
+      const unsigned long long now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > P.timeout_ns) {
+        raise_err_at(P, UZIP_ERR_TIMEOUT, 2, epoch, ld_acquire_sys_u64(cr), (uint64_t)(uintptr_t)cr);
+        return false;
+      }
+    }
+    __nanosleep(64);
+  }
+}
+
+// Decoupled look-back over the tiles of one stream, in two halves so the
+// aggregate can be published as soon as a tile is coded and the scan finished
+// later.  publish: one thread.  finish: one full warp; returns the exclusive
+// prefix of tile t, or ~0 on abort.
+__device__ __forceinline__ void lookback_publish(unsigned long long *status, uint64_t t, unsigned long long agg) {
+  st_relaxed_u64(&status[t], (t == 0 ? kFlagInc : kFlagAgg) | agg);
+}
+
+static __device__ unsigned long long lookback_finish(const Plan &P, unsigned long long *status, uint64_t t,
+                                              unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) return 0;
+  unsigned long long excl = 0, t0 = 0;
+  int64_t base = (int64_t)t - 1;
+  for (int spin = 0;; ++spin) {
+    const int64_t idx = base - lane;
+    unsigned long long s = idx >= 0 ? ld_relaxed_u64(&status[idx]) : (kFlagInc | 0ull);
+    const uint32_t flag = (uint32_t)(s >> 62);
+    const uint32_t inc = __ballot_sync(0xFFFFFFFFu, flag == 2);
+    const uint32_t notready = __ballot_sync(0xFFFFFFFFu, flag == 0);
+    const int first_inc = inc ? __ffs(inc) - 1 : 31;
+    const uint32_t needed = first_inc == 31 ? 0xFFFFFFFFu : ((2u << first_inc) - 1u);
+    if (notready & needed) {
+      if ((spin & 255) == 255) {
+        bool stop = false;
+        if (lane == 0) {
+          const unsigned long long now = globaltimer_ns();
+          if (ld_volatile_u32(P.err)) stop = true;
+          else if (t0 == 0) t0 = now;
+          else if (now - t0 > P.timeout_ns) {
+            raise_err_at(P, UZIP_ERR_TIMEOUT, 3, (uint32_t)t, s, (uint64_t)(uintptr_t)status);
+            stop = true;
+          }
+        }
+        if (__shfl_sync(0xFFFFFFFFu, stop, 0)) return ~0ull;
+      }
+      __nanosleep(32);
+      continue;
+    }
+    excl += warp_sum_u64(lane <= first_inc ? (s & kValMask) : 0ull);
+    if (inc) break;
+    base -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(&status[t], kFlagInc | (excl + agg));
+  return excl;
+}
+
+static __device__ unsigned long long lookback(const Plan &P, unsigned long long *status, uint64_t t,
+                                       unsigned long long agg) {
+  if ((threadIdx.x & 31) == 0) lookback_publish(status, t, agg);
+  return lookback_finish(P, status, t, agg);
+}
+
+// ---------------------------------------------------------------- fp32 fold helpers (a9, R11)
+template <int DT>
+__device__ __forceinline__ float widen(uint32_t bits) {
+  if (DT == kBF16) return __uint_as_float(bits << 16);
+  if (DT == kF16) return __half2float(__ushort_as_half((unsigned short)bits));
+  return __uint_as_float(bits);
+}
+template <int DT>
+__device__ __forceinline__ uint32_t narrow(float v) {
+  if (v != v) return DT == kF32 ? 0x7FFFFFFFu : 0x7FFFu;  // canonical NaN
+  if (DT == kBF16) return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v));
+  if (DT == kF16) return (uint32_t)__half_as_ushort(__float2half_rn(v));
+  return __float_as_uint(v);
+}
+__device__ __forceinline__ float fold(float acc, float x, bool first) { return first ? x : __fadd_rn(acc, x); }
+
+// Fold 16 bytes of elements into acc[0..kPer) (kPer = 8 for 2-byte types, 4 for fp32).
+template <int DT>
+__device__ __forceinline__ void fold_vec(float *acc, uint4 v, bool first) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if (DT == kF32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = fold(acc[i], widen<DT>(w[i]), first);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] = fold(acc[2 * i], widen<DT>(w[i] & 0xFFFFu), first);
+      acc[2 * i + 1] = fold(acc[2 * i + 1], widen<DT>(w[i] >> 16), first);
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ uint4 narrow_vec(const float *acc) {
+  uint4 o;
+  uint32_t *w = &o.x;
+  if (DT == kF32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = narrow<DT>(acc[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = narrow<DT>(acc[2 * i]) | (narrow<DT>(acc[2 * i + 1]) << 16);
+  }
+  return o;
+}
+
+// ================================================================ k_fused
+template <int DT, int B>
+struct FusedCfg {
+  static constexpr int kVec = (DT == kF32) ? 4 : 8;        // elements per 16-byte load
+  static constexpr int kIters = B / (32 * kVec);            // loads per lane per block
+  static constexpr int kBatch = kIters < 8 ? kIters : 8;
+  static constexpr int kRounds = B / 32;
+  static constexpr int kEncTab = 4096;                      // 256 x uint4
+  static constexpr int kWarpBuf = B + 256;                  // per warp: symbols/words (E) or payload + ring (D)
+  static constexpr int kDecTab = 4096 * 4;
+  static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce)
+  static constexpr int ring(bool red) { return red ? 0 : 16384; }  // coded tile awaiting its offset
+  static constexpr int smem(bool dec, bool red) {
+    return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0) + (red ? kWarps * kAcc : 0);
+  }
+};
+
+struct FusedShared {
+  uint32_t tk[2];
+  uint32_t abort;
+  uint32_t tile_cnt;
+  unsigned long long tile_off;
+  uint32_t size[kWarps], k[kWarps], ovf[kWarps];
+  uint32_t psize[kWarps], pkdir[kWarps];  // the pending (coded, offset unknown) tile
+  unsigned long long pagg, ptile_off;
+  unsigned long long prefix;
+  unsigned long long src_off[kMaxRanks];
+  unsigned long long src_payload[kMaxRanks];
+  uint32_t red[kWarps];
+};
+
+// ---------------------------------------------------------------- E item
+// Header (sizes before/after), zero pads and raw tail of a stream; one warp.
+template <int DT>
+static __device__ void finalize_stream(const EncJob &J, unsigned long long payload) {
+  const int lane = threadIdx.x & 31;
+  const StreamGeom &g = J.g;
+  const uint64_t total = g.total(payload);
+  if (lane == 0) {
+    uint32_t h[16];
+    for (int i = 0; i < 16; ++i) h[i] = 0;
+    h[0] = 0x31425A55u;  // "UZB1"
+    h[1] = kVersion | (g.dtype << 16) | ((g.global & 1u) << 24);
+    h[2] = (uint32_t)g.n;
+    h[3] = (uint32_t)(g.n >> 32);
+    h[4] = g.B;
+    h[5] = g.CB;
+    h[6] = g.S;
+    h[7] = kProbBits | (kLanes << 8) | (kLBits << 16);
+    h[8] = (uint32_t)g.n_blocks;
+    h[9] = (uint32_t)g.n_chunks;
+    h[10] = (uint32_t)payload;
+    h[11] = (uint32_t)(payload >> 32);
+    h[12] = (uint32_t)total;
+    h[13] = (uint32_t)(total >> 32);
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      uint4 *o = reinterpret_cast<uint4 *>(J.dst[d]);
+      for (int i = 0; i < 4; ++i) o[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+    }
+    if (J.d_out_bytes) *J.d_out_bytes = total;
+    if (J.wire_acc) atomicAdd(J.wire_acc, (unsigned long long)total * J.nd);
+  }
+  const uint64_t e1 = g.off_coff + 8 * g.n_chunks, e2 = g.off_dir + 4 * g.n_blocks;
+  const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+  const uint8_t *tsrc = J.in + g.n_coded * g.eb;
+  for (uint32_t d = 0; d < J.nd; ++d) {
+    uint8_t *o = J.dst[d];
+    for (uint64_t p = e1 + lane; p < g.off_dir; p += 32) o[p] = 0;
+    for (uint64_t p = e2 + lane; p < g.off_pay; p += 32) o[p] = 0;
+    uint8_t *tdst = o + g.off_tail(payload);
+    for (uint64_t i = lane; i < tail_bytes; i += 32) tdst[i] = tsrc[i];
+  }
+}
+
+// a1: split block b.  REV: symbol rows in coding order (row of round j at
+// (R-1-j)*32, lanes in order within a row) for the encoder; otherwise element
+// order (the stored-raw payload).  RES: also store the residual plane(s) to
+// every destination (split-send: they leave before the exponents are coded).
+template <int DT, int B, bool RES, bool REV, bool ND1>
+__device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
+                                              uint8_t *buf) {
+  using C = FusedCfg<DT, B>;
+  const int lane = threadIdx.x & 31;
+  // ND1: one destination (codec, P2P): the residual bases are computed once
+  uint8_t *r0 = J.dst[0] + g.off_res0 + (DT == kF32 ? 2 : 1) * (b * B);
+  uint8_t *r1 = J.dst[0] + g.off_res1 + b * B;
+  // byte of the lane's first vector in buf; later vectors of the lane step by kVec*32 elements (one row
+  // group), backwards in coding order (REV) -- an immediate offset in the store
+  const uint32_t e0 = (uint32_t)lane * C::kVec;
+  uint8_t *pos0 = buf + (REV ? (uint32_t)(B - 32) - (e0 & ~31u) + (e0 & 31u) : e0);
+#pragma unroll
+  for (int h = 0; h < C::kIters; h += C::kBatch) {
+    uint4 v[C::kBatch];
+#pragma unroll
+    for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
+#pragma unroll
+    for (int i = 0; i < C::kBatch; ++i) {
+      const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;  // element within block
+      uint8_t *sp = REV ? pos0 - 32 * C::kVec * (h + i) : pos0 + 32 * C::kVec * (h + i);
+      if (DT == kF32) {
+        uint32_t s4, h4;
+        uint2 lo;
+        split4_f32(v[i], s4, lo, h4);
+        *reinterpret_cast<uint32_t *>(sp) = s4;
+        if (RES) {
+          if (ND1) {
+            *reinterpret_cast<uint2 *>(r0 + 2 * e) = lo;
+            *reinterpret_cast<uint32_t *>(r1 + e) = h4;
+          } else {
+            for (uint32_t d = 0; d < J.nd; ++d) {
+              *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
+              *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
+            }
+          }
+        }
+      } else {
+        uint32_t s0, s1, q0, q1;
+        if (DT == kBF16) {
+          split4_bf16(v[i].x, v[i].y, s0, q0);
+          split4_bf16(v[i].z, v[i].w, s1, q1);
+        } else {
+          split4_f16(v[i].x, v[i].y, s0, q0);
+          split4_f16(v[i].z, v[i].w, s1, q1);
+        }
+        *reinterpret_cast<uint2 *>(sp) = make_uint2(s0, s1);
+        if (RES) {
+          if (ND1) {
+            *reinterpret_cast<uint2 *>(r0 + e) = make_uint2(q0, q1);
+          } else {
+            for (uint32_t d = 0; d < J.nd; ++d)
+              *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(q0, q1);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int DT, int B, bool RES, bool REV>
+__device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
+                                            uint8_t *buf) {
+  if (!RES || J.nd == 1) split_block_t<DT, B, RES, REV, true>(J, g, b, src, buf);
+  else split_block_t<DT, B, RES, REV, false>(J, g, b, src, buf);
+}
+
+// a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body); the
+// symbols and table entries of 8 rounds are loaded ahead of their math.
+// Words are compacted (ballot + popc) into emission order.  GLOBAL = false:
+// words go to buf, behind the rows already read (limit 16 words per consumed
+// row); a word that would overtake them sets `ovf` and is dropped.  GLOBAL =
+// true (rare path): words go straight to every destination at payload offset
+// `off` + 128.
+template <int DT, int B, bool GLOBAL>
+__device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &g, unsigned long long off,
+                                             uint8_t *buf, const uint4 *tab, uint32_t &x_out, uint32_t &K,
+                                             bool &ovf) {
+  using C = FusedCfg<DT, B>;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
+  uint32_t x = kL, wp = 0;
+  bool over = false;
+  constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
+  constexpr int kG = UZIP_ENC_GROUP;
+#pragma unroll 1
+  for (int G = 0; G < C::kRounds / kG; ++G) {
+    uint4 ent[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) ent[u] = tab[buf[(kG * G + u) * 32 + lane]];
+    __syncwarp();  // every lane read these rows before words may land in them
+    const uint32_t lim = GLOBAL ? kCap : min(kCap, (uint32_t)(16 * kG) * (G + 1));
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const uint4 e = ent[u];
+      const bool p = (x | 0x7FFFFu) >= e.y;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+      const uint32_t idx = min(wp + __popc(m & lt), lim - 1);  // clamped words are never used
+      if (GLOBAL) {
+        if (p && idx + 1 < kCap)
+          for (uint32_t d = 0; d < J.nd; ++d)
+            *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + 2 * idx) = (uint16_t)x;
+      } else if (p) {
+        buf16[idx] = (uint16_t)x;
+      }
+      x = p ? (x >> 16) : x;
+      wp += __popc(m);
+      const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
+      x = x + e.z + q * e.w;
+    }
+    over |= wp > lim;
+  }
+  x_out = x;
+  K = wp;
+  ovf = over;
+}
+
+// A coded tile whose payload waits in the CTA's ring for its offset: the
+// tile's aggregate is published as soon as it is coded, the look-back is
+// finished one tile later (when every predecessor has long been coded), so
+// warps never idle on stragglers.  Uniform across the CTA.
+struct EncPending {
+  int32_t job;  // -1: none
+  uint64_t t;
+};
+
+template <int DT, int B>
+static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint8_t *ring, EncPending &pd) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const EncJob &J = P.e[pd.job];
+  const StreamGeom &g = J.g;
+  const uint64_t t = pd.t;
+  pd.job = -1;
+  if (warp == 0) {
+    const unsigned long long excl = lookback_finish(P, J.tile_status, t, S.pagg);
+    if (lane == 0) S.ptile_off = excl;
+  }
+  __syncthreads();
+  const unsigned long long tile_off = S.ptile_off;
+  if (tile_off != ~0ull) {
+    const uint64_t b0 = t * kTileBlocks, b = b0 + warp;
+    const uint64_t c = b0 / g.CB;
+    uint32_t roff = 0;
+    for (int w = 0; w < warp; ++w) roff += S.psize[w];
+    const uint32_t size = S.psize[warp];
+    if (b < g.n_blocks) {
+      const unsigned long long off = tile_off + roff;
+      for (uint32_t d = 0; d < J.nd; ++d) {
+        if (lane == 0) {
+          reinterpret_cast<uint32_t *>(J.dst[d] + g.off_dir)[b] = S.pkdir[warp];
+          if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[b / g.CB] = off;
+        }
+        uint4 *o = reinterpret_cast<uint4 *>(J.dst[d] + g.off_pay + off);
+        for (uint32_t i = lane; i < size / 16; i += 32) o[i] = reinterpret_cast<const uint4 *>(ring + roff)[i];
+      }
+      if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
+    }
+    if (b0 % g.CB == 0 && warp == kWarps - 1) {  // the chunk's first tile carries its table
+      const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
+      for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
+    }
+    bool flags = false;
+    for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+    if (flags) {
+      __syncwarp();
+      if (lane == 0) {
+        // every warp fences its own stores at system scope before counting in (a CTA-scope fence
+        // + one system fence by the last warp was measured to lose tiles in the loopback bench)
+        __threadfence_system();
+        if (atomicAdd(&S.tile_cnt, 1u) == kWarps - 1) {
+          S.tile_cnt = 0;
+          const unsigned long long off16 = tile_off >> 4;
+          for (uint32_t d = 0; d < J.nd; ++d)
+            if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+        }
+      }
+    }
+  }
+  __syncthreads();  // the ring and the pending sizes are free again
+}
+
+// One encode tile: every warp codes one block; one warp finds the tile's
+// offset by decoupled look-back over tiles; the last warp of the tile to
+// finish its stores releases the tile's flags.
+template <int DT, int B>
+static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &enc_key, uint32_t &credit_done, uint8_t *ring, int ring_bytes, EncPending &pd) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
+    if (tid == 0) {
+      uint32_t ok = 1;
+      for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
+      S.abort = ok ? 0u : 1u;
+    }
+    __syncthreads();
+    if (S.abort) return;
+    credit_done |= 1u << jidx;
+  }
+  bool flags = false;
+  for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+
+  if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256) {
+      const uint4 v = ldg_nc_v4(J.in + o0 + 16 * i);
+      for (uint32_t d = 0; d < J.nd; ++d) *reinterpret_cast<uint4 *>(J.dst[d] + o0 + 16 * i) = v;
+    }
+    for (uint64_t i = nv * 16 + tid; i < len; i += 256) {
+      const uint8_t v = J.in[o0 + i];
+      for (uint32_t d = 0; d < J.nd; ++d) J.dst[d][o0 + i] = v;
+    }
+    __syncthreads();
+    if (tid == 0 && flags) {
+      __threadfence_system();
+      for (uint32_t d = 0; d < J.nd; ++d)
+        if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
+    }
+    return;
+  }
+
+  const StreamGeom &g = J.g;
+  uint4 *tab = reinterpret_cast<uint4 *>(smem);
+  // One B-byte buffer per warp: symbol rows stored in coding order (round R-1
+  // first); the coded words grow from byte 0 into the rows already consumed.
+  uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t key = ((uint64_t)jidx << 48) | c;
+  if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
+    tab[tid] = J.enc[c * 256 + tid];
+    enc_key = key;
+    __syncthreads();
+  }
+
+  const uint64_t b = b0 + warp;
+  const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
+  uint32_t size = 0, kdir = 0, K = 0, x = kL;
+  bool raw = false, ovf = false;
+  if (b < g.n_blocks) {
+    // ---- a1: split; the residual goes straight to every destination (split-send)
+    split_block<DT, B, true, true>(J, g, b, src, buf);
+    __syncwarp();
+    encode_block<DT, B, false>(J, g, 0, buf, tab, x, K, ovf);
+    const uint32_t coded = (uint32_t)round16(128 + 2ull * K);
+    raw = coded >= (uint32_t)B;  // stored raw (R13)
+    size = raw ? (uint32_t)B : coded;
+    kdir = raw ? kRawBlock : K;
+    __syncwarp();
+    if (raw) {
+      split_block<DT, B, false, false>(J, g, b, src, buf);  // payload = the symbols in element order
+    } else if (!ovf && lane < 8) {
+      buf16[K + lane] = 0;  // zero pad up to the 16-byte boundary (K + 8 <= kCap + 8 words fit)
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    S.size[warp] = size;
+    S.ovf[warp] = (ovf && !raw) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);  // the previous tile's offset is due now
+
+  // ---- a5: tile prefix by decoupled look-back
+  uint32_t sum = 0, roff = 0, anyovf = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) roff += S.size[w];
+    sum += S.size[w];
+    anyovf |= S.ovf[w];
+  }
+  if (g.n_blocks && !anyovf && sum <= (uint32_t)ring_bytes) {
+    // park the coded tile in the ring, publish its aggregate, go on coding
+    if (b < g.n_blocks) {
+      uint8_t *r = ring + roff;
+      if (raw) {
+        for (uint32_t i = lane; i < size / 16; i += 32)
+          reinterpret_cast<uint4 *>(r)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      } else {
+        reinterpret_cast<uint32_t *>(r)[lane] = x;
+        for (uint32_t i = lane; i < (size - 128) / 16; i += 32)
+          reinterpret_cast<uint4 *>(r + 128)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      }
+    }
+    if (lane == 0) {
+      S.psize[warp] = size;
+      S.pkdir[warp] = kdir;
+    }
+    if (tid == 0) {
+      S.pagg = sum;
+      lookback_publish(J.tile_status, t, sum);
+    }
+    pd.job = jidx;
+    pd.t = t;
+    return;  // the item-end barrier publishes the ring contents to the resolving warps
+  }
+  if (warp == 0) {
+    const unsigned long long excl = lookback(P, J.tile_status, t, sum);
+    if (lane == 0) S.tile_off = excl;
+  }
+  __syncthreads();
+  const unsigned long long tile_off = S.tile_off;
+  if (tile_off == ~0ull) return;  // aborted (timeout / peer error)
+
+  if (b < g.n_blocks) {
+    unsigned long long off = tile_off;
+    for (int w = 0; w < warp; ++w) off += S.size[w];
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      uint8_t *o = J.dst[d] + g.off_pay + off;
+      if (lane == 0) {
+        reinterpret_cast<uint32_t *>(J.dst[d] + g.off_dir)[b] = kdir;
+        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[b / g.CB] = off;
+      }
+      if (raw) {
+        for (uint32_t i = lane; i < size / 16; i += 32)
+          reinterpret_cast<uint4 *>(o)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      } else {
+        reinterpret_cast<uint32_t *>(o)[lane] = x;  // the block header: 32 final lane states
+        if (!ovf)
+          for (uint32_t i = lane; i < (size - 128) / 16; i += 32)
+            reinterpret_cast<uint4 *>(o + 128)[i] = reinterpret_cast<const uint4 *>(buf)[i];
+      }
+    }
+    if (ovf && !raw) {
+      // rare: the words outran the consumed symbol rows -- code the block again,
+      // now storing each word straight to its final place (offset known)
+      __syncwarp();
+      split_block<DT, B, false, true>(J, g, b, src, buf);
+      __syncwarp();
+      uint32_t x2 = kL, K2 = 0;
+      bool o2 = false;
+      encode_block<DT, B, true>(J, g, off, buf, tab, x2, K2, o2);
+      for (uint32_t d = 0; d < J.nd; ++d)
+        for (uint32_t i = 2 * K + lane * 2; i < size - 128; i += 64)
+          *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + i) = 0;
+    }
+    if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
+  } else if (g.n_blocks == 0 && warp == 0) {  // no whole block: header + raw tail only
+    finalize_stream<DT>(J, 0ull);
+  }
+  // the chunk's first tile carries its serialized table (the receiver waits for it)
+  if (g.n_blocks && b0 % g.CB == 0 && warp == kWarps - 1) {
+    const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
+    for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
+  }
+  if (flags) {  // the last warp of the tile to finish its stores releases the tile's flags (a12)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_system();
+      if (atomicAdd(&S.tile_cnt, 1u) == kWarps - 1) {
+        S.tile_cnt = 0;
+        const unsigned long long off16 = tile_off >> 4;
+        for (uint32_t d = 0; d < J.nd; ++d)
+          if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- C item
+static __device__ void copy_item(const CopyJob &Cj, uint64_t t) {
+  const uint64_t o0 = t * kRawTileBytes;
+  const uint64_t len = min((uint64_t)kRawTileBytes, Cj.bytes - o0);
+  const uint64_t nv = len / 16;
+  for (uint64_t i = threadIdx.x; i < nv; i += 256)
+    st_any16(Cj.dst + o0 + 16 * i, ldg_nc_v4(Cj.src + o0 + 16 * i));
+  for (uint64_t i = nv * 16 + threadIdx.x; i < len; i += 256) Cj.dst[o0 + i] = Cj.src[o0 + i];
+}
+
+// Completion of one D item: the last tile of the job releases the sources' slots.
+static __device__ void dec_done(const DecJob &J) {
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  const uint32_t old = atomicAdd(J.done, 1u);
+  if (old == (uint32_t)J.ntiles - 1) {
+    __threadfence();
+    *J.done = 0;
+    for (uint32_t s = 0; s < J.nsrc; ++s)
+      if ((int32_t)s != J.me && J.credit[s]) st_release_sys_u64(J.credit[s], (unsigned long long)J.epoch[s]);
+  }
+}
+
+// Thread 0: acquire tile t of source s (and the chunk's first tile, which
+// carries the table, when the table is not cached).  Sets S.abort on failure.
+static __device__ void acquire_tile(const Plan &P, const DecJob &J, uint32_t s, uint64_t t, bool need_table,
+                             FusedShared &S) {
+  unsigned long long v = 0;
+  bool ok = wait_flag(P, J.flag[s] + t, J.epoch[s], v);
+  S.src_off[s] = (v & 0xFFFFFFFFull) << 4;
+  if (ok && need_table && !J.raw && J.g.n_blocks) {
+    const uint64_t first = (t * kTileBlocks / J.g.CB) * J.g.CB / kTileBlocks;
+    if (first != t) {
+      unsigned long long v2;
+      ok = wait_flag(P, J.flag[s] + first, J.epoch[s], v2);
+    }
+  }
+  S.abort = ok ? 0u : 1u;
+}
+
+// Per-block payload offsets within a tile from the directory (all lanes of a warp).
+__device__ __forceinline__ void tile_block(const uint8_t *stream, const StreamGeom &g, uint64_t b0, int warp,
+                                           unsigned long long tile_off, uint32_t &K, unsigned long long &off,
+                                           unsigned long long &tile_end, bool &bad) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t *dir = reinterpret_cast<const uint32_t *>(stream + g.off_dir);
+  uint32_t d = 0, sz = 0;
+  bool bb = false;
+  if (lane < kWarps && b0 + lane < g.n_blocks) {
+    d = ld_cg_u32c(dir + b0 + lane);
+    sz = block_size(d, g.B, bb);
+  }
+  bad = __any_sync(0xFFFFFFFFu, bb);
+  uint32_t incl = sz;
+  for (int o = 1; o < 8; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  K = __shfl_sync(0xFFFFFFFFu, d, warp);
+  off = tile_off + __shfl_sync(0xFFFFFFFFu, incl - sz, warp);
+  tile_end = tile_off + __shfl_sync(0xFFFFFFFFu, incl, kWarps - 1);
+}
+
+// Stage block payload into smem (warp).
+__device__ __forceinline__ void stage_payload(const uint8_t *stream, const StreamGeom &g, unsigned long long off,
+                                              uint32_t size, uint8_t *pay) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t *p = stream + g.off_pay + off;
+  for (uint32_t i = lane; i < size / 16; i += 32) reinterpret_cast<uint4 *>(pay)[i] = ld_cg_v4(p + 16 * i);
+  __syncwarp();
+}
+
+// Copy stream bytes [o, o+len) from the local staging to the same offset in
+// every forward destination (all threads of the CTA).
+__device__ __forceinline__ void fwd_range(const DecJob &J, const uint8_t *stream, uint64_t o, uint64_t len) {
+  const uint64_t nv = len / 16;
+  for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    const uint4 v = ld_cg_v4(stream + o + 16 * i);
+    for (uint32_t d = 0; d < J.nfwd; ++d) *reinterpret_cast<uint4 *>(J.fdst[d] + o + 16 * i) = v;
+  }
+  for (uint64_t i = nv * 16 + threadIdx.x; i < len; i += blockDim.x) {
+    const uint8_t v = stream[o + i];
+    for (uint32_t d = 0; d < J.nfwd; ++d) J.fdst[d][o + i] = v;
+  }
+}
+
+// Relay of one received tile (broadcast): the bytes the tile's flag covers --
+// residual plane(s), directory entries, payload range, the chunk's table and
+// offset on its first tile, header/pads/tail on the last -- are stored as
+// received into the next hops' staging, then their flags are released with
+// the same payload offset.  No decode, no re-encode.
+template <int DT>
+static __device__ void forward_tile(const Plan &P, const DecJob &J, uint64_t t, FusedShared &S, uint32_t &fwd_done,
+                             int jidx) {
+  const int tid = threadIdx.x;
+  const StreamGeom &g = J.g;
+  const uint8_t *stream = J.src[0];
+  if (!((fwd_done >> jidx) & 1u)) {  // first forward of this job in this CTA: the hops' slots are free
+    if (tid == 0) {
+      uint32_t ok = 1;
+      for (uint32_t d = 0; d < J.nfwd && ok; ++d) ok = wait_credit(P, J.fcredit[d], J.fepoch[d]);
+      S.abort = ok ? 0u : 1u;
+    }
+    __syncthreads();
+    if (S.abort) return;
+    fwd_done |= 1u << jidx;
+  }
+  const unsigned long long tile_off = S.src_off[0];
+  if (warp_id() == 0) {
+    uint32_t K;
+    unsigned long long off, tile_end;
+    bool bad;
+    tile_block(stream, g, t * kTileBlocks, 0, tile_off, K, off, tile_end, bad);
+    if ((threadIdx.x & 31) == 0) S.ptile_off = bad ? tile_off : tile_end;
+  }
+  __syncthreads();
+  const unsigned long long tile_end = S.ptile_off;
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t nblk = g.n_blocks > b0 ? min((uint64_t)kTileBlocks, g.n_blocks - b0) : 0;
+  if (nblk) {
+    if (DT == kF32) {
+      fwd_range(J, stream, g.off_res0 + 2 * b0 * g.B, 2 * nblk * g.B);
+      fwd_range(J, stream, g.off_res1 + b0 * g.B, nblk * g.B);
+    } else {
+      fwd_range(J, stream, g.off_res0 + b0 * g.B, nblk * g.B);
+    }
+    fwd_range(J, stream, g.off_dir + 4 * b0, 4 * nblk);
+    fwd_range(J, stream, g.off_pay + tile_off, tile_end - tile_off);
+    if (b0 % g.CB == 0) {
+      const uint64_t c = b0 / g.CB;
+      fwd_range(J, stream, g.off_tab + 512 * c, 512);
+      fwd_range(J, stream, g.off_coff + 8 * c, 8);
+    }
+  }
+  if (t == J.ntiles - 1) {  // header, section pads, raw tail
+    fwd_range(J, stream, 0, kHeaderBytes);
+    fwd_range(J, stream, g.off_coff + 8 * g.n_chunks, g.off_dir - (g.off_coff + 8 * g.n_chunks));
+    fwd_range(J, stream, g.off_dir + 4 * g.n_blocks, g.off_pay - (g.off_dir + 4 * g.n_blocks));
+    fwd_range(J, stream, g.off_tail(tile_end), (g.n - g.n_coded) * g.eb);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (uint32_t d = 0; d < J.nfwd; ++d)
+      st_release_sys_u64(J.fflag[d] + t, ((unsigned long long)J.fepoch[d] << 32) | (tile_off >> 4));
+  }
+}
+
+// ---------------------------------------------------------------- D item: decode (+ join)
+template <int DT, int B, bool RED>
+static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &dec_key, uint32_t &fwd_done) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, warp = warp_id();
+  const StreamGeom &g = J.g;
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t key = (1ull << 63) | ((uint64_t)jidx << 48) | c;
+  const bool need_table = key != dec_key;
+  if (tid == 0) acquire_tile(P, J, 0, t, need_table, S);
+  __syncthreads();
+  if (S.abort) return;
+  const uint8_t *stream = J.src[0];
+  if (J.raw) {
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256)
+      st_any16(J.out + o0 + 16 * i, ld_cg_v4(stream + o0 + 16 * i));
+    for (uint64_t i = nv * 16 + tid; i < len; i += 256) J.out[o0 + i] = stream[o0 + i];
+    __syncthreads();
+    dec_done(J);
+    return;
+  }
+  if (J.nfwd) {  // relay first: the next hops receive the tile before it is decoded here
+    forward_tile<DT>(P, J, t, S, fwd_done, jidx);
+    if (S.abort) return;
+  }
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + P.ring_bytes);
+  if (g.n_blocks && need_table) {
+    if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
+      if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+      dec_key = ~0ull;
+      return;
+    }
+    dec_key = key;
+  }
+  __syncthreads();
+  uint8_t *pay = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint8_t *symb = pay + B;
+  const uint64_t b = b0 + warp;
+  uint32_t K;
+  unsigned long long off, tile_end;
+  bool bad;
+  tile_block(stream, g, b0, warp, S.src_off[0], K, off, tile_end, bad);
+  if (b < g.n_blocks && !bad) {
+    const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
+    stage_payload(stream, g, off, size, pay);
+    uint8_t *dst = J.out + b * (uint64_t)B * g.eb;
+    if (K == kRawBlock) join_block<DT, B>(pay, stream, g, b, dst);
+    else if (!decode_join_warp<DT, B>(pay, K, dtab, symb, stream, g, b, dst)) bad = true;
+    __syncwarp();
+  }
+  if (bad && (threadIdx.x & 31) == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+  if (t == J.ntiles - 1) {  // raw tail
+    const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+    const uint8_t *tsrc = stream + g.off_tail(tile_end);
+    uint8_t *tdst = J.out + g.n_coded * g.eb;
+    for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
+  }
+  __syncthreads();
+  dec_done(J);
+}
+
+// Epilogue that folds a decoded source into the warp's fp32 accumulator (a9).
+struct FoldEpi {
+  float *acc;
+  bool first;
+  template <int DT>
+  __device__ __forceinline__ void apply(uint32_t e0, uint4 a, uint4 b) const {
+    float v[8];
+    if (!first)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = acc[e0 + i];
+    if (DT == kF32) {
+      fold_vec<DT>(v, a, first);
+      fold_vec<DT>(v + 4, b, first);
+    } else {
+      fold_vec<DT>(v, a, first);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[e0 + i] = v[i];
+  }
+};
+
+// ---------------------------------------------------------------- D item: decode + reduce (a9)
+template <int DT, int B>
+static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &dec_key) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const StreamGeom &g = J.g;
+  const uint32_t eb = elem_bytes(DT);
+  constexpr int kPer = C::kVec;
+
+  if (J.raw) {  // ---- below the threshold: fold raw tiles
+    for (uint32_t s = 0; s < J.nsrc; ++s) {
+      if ((int32_t)s == J.me) continue;
+      if (tid == 0) acquire_tile(P, J, s, t, false, S);
+      __syncthreads();
+      if (S.abort) return;
+    }
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256) {
+      float acc[8];
+      for (uint32_t s = 0; s < J.nsrc; ++s) {
+        const uint8_t *p = J.src[s] + o0 + 16 * i;
+        const uint4 v = ((int32_t)s == J.me) ? ldg_nc_v4(p) : ld_cg_v4(p);
+        fold_vec<DT>(acc, v, s == 0);
+      }
+      *reinterpret_cast<uint4 *>(J.out + o0 + 16 * i) = narrow_vec<DT>(acc);
+    }
+    for (uint64_t i = nv * 16 / eb + tid; i < len / eb; i += 256) {  // scalar tail
+      float acc = 0.f;
+      for (uint32_t s = 0; s < J.nsrc; ++s) {
+        const uint8_t *p = J.src[s] + o0 + i * eb;
+        const uint32_t bits = DT == kF32 ? *reinterpret_cast<const uint32_t *>(p)
+                                         : (uint32_t)*reinterpret_cast<const uint16_t *>(p);
+        acc = fold(acc, widen<DT>(bits), s == 0);
+      }
+      const uint32_t r = narrow<DT>(acc);
+      if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + o0 + i * eb) = r;
+      else *reinterpret_cast<uint16_t *>(J.out + o0 + i * eb) = (uint16_t)r;
+    }
+    __syncthreads();
+    dec_done(J);
+    return;
+  }
+
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t b = b0 + warp;
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true));
+  float *acc = reinterpret_cast<float *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true) + C::kDecTab) + warp * B;
+  uint8_t *pay = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint8_t *symb = pay + B;
+  bool bad = false;
+
+  for (uint32_t s = 0; s < J.nsrc; ++s) {
+    const bool first = s == 0;
+    if ((int32_t)s == J.me) {  // own shard: never compressed
+      if (b < g.n_blocks) {
+        const uint8_t *src = J.src[s] + b * (uint64_t)B * eb;
+        for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer) {
+          float a[8];
+          if (!first)
+            for (int i = 0; i < kPer; ++i) a[i] = acc[e + i];
+          fold_vec<DT>(a, ldg_nc_v4(src + e * eb), first);
+          for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    const uint64_t key = (2ull << 62) | ((uint64_t)jidx << 48) | ((uint64_t)s << 40) | c;
+    const bool need_table = key != dec_key;
+    if (tid == 0) acquire_tile(P, J, s, t, need_table, S);
+    __syncthreads();
+    if (S.abort) return;
+    const uint8_t *stream = J.src[s];
+    if (g.n_blocks && need_table) {
+      if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
+        if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+        dec_key = ~0ull;
+        return;
+      }
+      dec_key = key;
+    }
+    __syncthreads();
+    uint32_t K;
+    unsigned long long off, tile_end;
+    bool tb;
+    tile_block(stream, g, b0, warp, S.src_off[s], K, off, tile_end, tb);
+    bad |= tb;
+    if (tid == 0) S.src_payload[s] = tile_end;
+    if (b < g.n_blocks && !tb) {
+      const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
+      stage_payload(stream, g, off, size, pay);
+      FoldEpi epi{acc, first};
+      if (K != kRawBlock) {
+        if (!decode_join_warp_epi<DT, B>(pay, K, dtab, symb, stream, g, b, epi)) bad = true;
+      } else {  // stored-raw block: symbols are the payload
+        for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
+          const uint2 s8 = *reinterpret_cast<const uint2 *>(pay + e);
+          if (DT == kF32) {
+            const uint4 lo = ld_cg_v4(stream + g.off_res0 + 2 * (b * B + e));
+            const uint2 hi = ld_cg_v2(stream + g.off_res1 + b * B + e);
+            epi.template apply<DT>(e, join4_f32(s8.x, make_uint2(lo.x, lo.y), hi.x),
+                                   join4_f32(s8.y, make_uint2(lo.z, lo.w), hi.y));
+          } else {
+            const uint2 r8 = ld_cg_v2(stream + g.off_res0 + b * B + e);
+            uint4 v;
+            if (DT == kBF16) {
+              join4_bf16(s8.x, r8.x, v.x, v.y);
+              join4_bf16(s8.y, r8.y, v.z, v.w);
+            } else {
+              join4_f16(s8.x, r8.x, v.x, v.y);
+              join4_f16(s8.y, r8.y, v.z, v.w);
+            }
+            epi.template apply<DT>(e, v, v);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (bad && lane == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+  if (b < g.n_blocks) {  // one rounding to the dtype, 128-bit stores
+    uint8_t *dst = J.out + b * (uint64_t)B * eb;
+    for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer)
+      *reinterpret_cast<uint4 *>(dst + e * eb) = narrow_vec<DT>(acc + e);
+  }
+  __syncthreads();
+  if (t == J.ntiles - 1) {  // raw tails of every source, folded in rank order
+    const uint64_t tail = g.n - g.n_coded;
+    for (uint64_t i = tid; i < tail; i += 256) {
+      float a = 0.f;
+      for (uint32_t s = 0; s < J.nsrc; ++s) {
+        const uint8_t *p = ((int32_t)s == J.me) ? J.src[s] + (g.n_coded + i) * eb
+                                                : J.src[s] + g.off_tail(S.src_payload[s]) + i * eb;
+        const uint32_t bits = DT == kF32 ? *reinterpret_cast<const uint32_t *>(p)
+                                         : (uint32_t)*reinterpret_cast<const uint16_t *>(p);
+        a = fold(a, widen<DT>(bits), s == 0);
+      }
+      const uint32_t r = narrow<DT>(a);
+      if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + (g.n_coded + i) * eb) = r;
+      else *reinterpret_cast<uint16_t *>(J.out + (g.n_coded + i) * eb) = (uint16_t)r;
+    }
+  }
+  __syncthreads();
+  dec_done(J);
+}
+
+// ---------------------------------------------------------------- the kernel
+// MINB: resident CTAs per SM the register allocation targets.  Launches with
+// encode items use UZIP_ENC_MINB (3: 85 registers, measured fastest for the
+// encoder); decode-only launches use 4 (64 registers, like k_decode).
+template <int DT, int B, bool RED, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Plan P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ FusedShared S;
+  const int tid = threadIdx.x;
+  uint64_t enc_key = ~0ull, dec_key = ~0ull;
+  uint32_t credit_done = 0, fwd_done = 0;
+  using Cf = FusedCfg<DT, B>;
+  uint8_t *ring = smem + Cf::kEncTab + kWarps * Cf::kWarpBuf;
+  EncPending pd{-1, 0};
+  const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
+  if (tid == 0) {
+    S.tile_cnt = 0;
+    S.tk[0] = atomicAdd(P.ticket, 1u);
+  }
+  __syncthreads();
+  uint64_t it = uniform_u64(S.tk[0]);
+  for (int par = 0; it < total; par ^= 1) {
+    if (tid == 0) S.tk[par ^ 1] = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
+    const bool coded_e = it < ne && !P.e[it % (uint64_t)P.ne].raw;
+    if (pd.job >= 0 && !coded_e) resolve_pending<DT, B>(P, S, ring, pd);
+    if (it < ne) {
+      const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
+      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, ring, P.ring_bytes, pd);
+    } else if (it < ne + nc) {
+      copy_item(P.c, it - ne);
+    } else {
+      uint64_t k = it - ne - nc;  // job-major over the decode jobs
+      int j = 0;
+      while (j + 1 < P.nd_jobs && k >= P.d[j].ntiles) k -= P.d[j++].ntiles;
+      if (RED && P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
+      else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
+    }
+    __syncthreads();
+    it = uniform_u64(S.tk[par ^ 1]);
+  }
+  if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);
+  if (tid == 0) {  // the last CTA out resets the ticket for the next launch
+    __threadfence();
+    if (atomicAdd(P.ticket + 1, 1u) == gridDim.x - 1) {
+      P.ticket[0] = 0;
+      P.ticket[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ================================================================ launchers
+inline int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int DT>
+cudaError_t launch_tables_t(const Plan &p, cudaStream_t st) {
+  uint64_t max_chunks = 1;  // >= 1: the look-back words are reset even without chunks
+  uint32_t max_parts = 1;
+  for (int j = 0; j < p.ne; ++j) {
+    const EncJob &J = p.e[j];
+    if (J.raw) continue;
+    max_chunks = J.g.n_chunks > max_chunks ? J.g.n_chunks : max_chunks;
+    for (uint64_t c = 0; c < J.g.n_chunks; c += (J.g.n_chunks > 1 ? J.g.n_chunks - 1 : 1)) {
+      const uint32_t parts = hist_parts(J.g.sample_len(c));
+      max_parts = parts > max_parts ? parts : max_parts;
+    }
+  }
+  k_hist<DT><<<dim3(max_parts, (unsigned)max_chunks, (unsigned)p.ne), kHistThreads, 0, st>>>(p);
+  k_norm<DT><<<dim3((unsigned)max_chunks, (unsigned)p.ne), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, int B, bool RED, int MINB>
+cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
+  using C = FusedCfg<DT, B>;
+  const bool dec = p.n_d_items > 0;
+  // the ring parks coded tiles (encode launches only; none in the reduce variant)
+  p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
+  const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0) +
+                   (RED ? kWarps * C::kAcc : 0);
+  auto kern = k_fused<DT, B, RED, MINB>;
+  static int attr_set = 0;
+  if (attr_set < C::smem(true, RED)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(true, RED));
+    attr_set = C::smem(true, RED);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  if (occ <= 0) occ = 1;
+  const uint64_t items = p.n_e_items + p.n_c_items + p.n_d_items;
+  int grid = sm_count() * occ;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if ((uint64_t)grid > items) grid = (int)(items ? items : 1);
+  kern<<<grid, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, int B, bool RED>
+cudaError_t launch_fused_t(const Plan &p, cudaStream_t st, int max_ctas) {
+  if constexpr (RED) {
+    return launch_fused_k<DT, B, RED, 1>(p, st, max_ctas);
+  } else {
+    if (p.n_e_items > 0) return launch_fused_k<DT, B, RED, UZIP_ENC_MINB>(p, st, max_ctas);
+    return launch_fused_k<DT, B, RED, 4>(p, st, max_ctas);
+  }
+}
+
+// Load every kernel of this dtype/variant into the context now.  CUDA's lazy
+// module loading synchronises the context when a kernel is first launched; a
+// communicator whose peer kernels spin-wait inside the same context (loopback
+// ranks) would then wait for a kernel that waits for it -- measured as a
+// 5 s poll timeout in the loopback bench -- so communicators preload.
+template <int DT, bool RED>
+cudaError_t preload_t() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaSuccess;
+  if constexpr (RED) {
+    e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, true, 1>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, true, 1>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, true, 1>);
+  } else {
+    e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_ENC_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_ENC_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, UZIP_ENC_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_hist<DT>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_norm<DT>);
+  }
+  return e;
+}
+
+template <int DT, bool RED>
+cudaError_t launch_fused_b(const Plan &p, uint32_t B, cudaStream_t st, int max_ctas) {
+  switch (B) {
+    case 1024: return launch_fused_t<DT, 1024, RED>(p, st, max_ctas);
+    case 2048: return launch_fused_t<DT, 2048, RED>(p, st, max_ctas);
+    default: return launch_fused_t<DT, 4096, RED>(p, st, max_ctas);
+  }
+}
+
+}  // namespace uzip

@@ -120,6 +120,7 @@ struct EncWs {
 static_assert(sizeof(Plan) <= 30000, "kernel parameter space");
 
 cudaError_t launch_tables(int dtype, const Plan &p, cudaStream_t st);
+cudaError_t preload_kernels();  // per device: defeat lazy loading for spin-waiting kernels
 cudaError_t launch_fused(int dtype, const Plan &p, cudaStream_t st, int max_ctas);
 
 }  // namespace uzip

@@ -1,0 +1,19 @@
+#!/bin/bash
+# compute-sanitizer passes (memcheck, racecheck, synccheck) over small codec and collective cases.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+python -c "from paper_2604_17172_b200 import _build; _build.build()" > /dev/null 2>&1
+SEL_CODEC='tests/test_gpu_codec.py::test_stream_bytes_equal_oracle'
+K_CODEC='W and 163845'
+SEL_COMM='tests/test_gpu_comm.py::test_p2p_bit_exact tests/test_gpu_comm.py::test_allreduce'
+K_COMM='(12305 and 0) or (W-0-2)'
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
+    python -m pytest $SEL_CODEC -k "$K_CODEC" -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_codec.log 2>&1
+  echo "$tool codec rc=$?" >> gpurun_out/sanitize_summary.txt
+  timeout 900 compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
+    python -m pytest $SEL_COMM -k "$K_COMM" -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_comm.log 2>&1
+  echo "$tool comm rc=$?" >> gpurun_out/sanitize_summary.txt
+done
+for f in gpurun_out/sanitize_*.log; do echo "== $f"; grep -E "ERROR SUMMARY|passed|failed|Error" $f | tail -4; done >> gpurun_out/sanitize_summary.txt
+cat gpurun_out/sanitize_summary.txt

@@ -1,0 +1,12 @@
+#!/bin/bash
+# Tuning: the same 1 GiB codec bench against libuzip variants (paper_2604_17172_b200/variants/*.so).
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+python -c "from paper_2604_17172_b200 import _build; _build.build()" > /dev/null 2>&1
+for v in default paper_2604_17172_b200/variants/*.so; do
+  for rep in 1 2; do
+    if [ "$v" = default ]; then L=""; else L="$PWD/$v"; fi
+    UZIP_LIB_PATH=$L timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-loopback 2>/dev/null | \
+      python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$v', d['encode']['ms'], d['decode']['ms'], d['value'])"
+  done
+done

@@ -323,3 +323,51 @@ def test_alltoall(uz, nr, dtype):
                 assert np.array_equal(host(outs[r], dtype), ref), r
     finally:
         g.close()
+
+
+def test_missing_peer_times_out_instead_of_hanging(uz):
+    """Failure detection: a recv whose sender never comes raises UZIP_ERR_TIMEOUT in the
+    communicator's async error word after poll_timeout_ms; the kernel exits, the GPU stays usable."""
+    import time
+    g = Group(uz, 2, staging_bytes=4 << 20, min_compress_bytes=1, poll_timeout_ms=300)
+    try:
+        y = torch.empty(1 << 20, dtype=torch.bfloat16, device="cuda")
+        t0 = time.time()
+        g.comms[1].recv(y, 0, g.streams[1])
+        torch.cuda.synchronize()
+        assert time.time() - t0 < 30
+        assert g.comms[1].async_error() == uz.ERR_TIMEOUT
+        # the device is fine: a plain codec call still works
+        x = torch.randn(4096 * 3, device="cuda").to(torch.bfloat16)
+        out, nb = uz.compress(x)
+        back, st = uz.decompress(out, x.numel(), uz.BF16)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0 and torch.equal(back.view(torch.int16), x.view(torch.int16))
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("max_ctas", [296, 1000])
+def test_p2p_large_full_occupancy(uz, max_ctas):
+    """The bench's loopback configuration: large multi-round message, both ranks' persistent kernels
+    as wide as the GPU allows (sender and receiver compete for SMs)."""
+    g = Group(uz, 2, staging_bytes=256 << 20, max_ctas=max_ctas, poll_timeout_ms=5000)
+    try:
+        n = 192 << 20  # 384 MiB bf16: several rounds through 128 MiB slots
+        gg = torch.Generator(device="cuda")
+        gg.manual_seed(5)
+        x = (torch.randn(n, device="cuda", generator=gg) * 0.02).to(torch.bfloat16)
+        y = torch.empty_like(x)
+        for _ in range(3):
+            y.fill_(0)
+            torch.cuda.synchronize()
+            g.comms[0].send(x, 1, g.streams[0])
+            g.comms[1].recv(y, 0, g.streams[1])
+            torch.cuda.synchronize()
+            errs = [c.async_error() for c in g.comms]
+            if errs != [0, 0]:
+                print("ERROR_DETAIL", [c.error_detail() for c in g.comms], flush=True)
+            assert errs == [0, 0]
+            assert torch.equal(x.view(torch.int16), y.view(torch.int16))
+    finally:
+        g.close()
