@@ -230,8 +230,9 @@ def run_codec(args):
     dec_bytes = total + raw           # read stream, write output
     enc_gbs = enc_bytes / (enc_ms / 1e3) / GB
     dec_gbs = dec_bytes / (dec_ms / 1e3) / GB
-    dom = ("k_table+k_encode (uzip_compress)", enc_gbs, enc_bytes) if enc_ms >= dec_ms else \
+    dom = ("k_hist+k_norm+k_fused (uzip_compress)", enc_gbs, enc_bytes) if enc_ms >= dec_ms else \
         ("k_decode (uzip_decompress)", dec_gbs, dec_bytes)
+    traffic = ncu_traffic(["k_hist", "k_norm", "k_fused"] if enc_ms >= dec_ms else ["k_decode"], args.bytes)
 
     # memcpy reference on the same box (context): torch copy_ of the same bytes
     z = torch.empty_like(x)
@@ -261,7 +262,7 @@ def run_codec(args):
         "decode": {"ms": round(dec_ms, 4), "uncompressed_GBps": round(raw / (dec_ms / 1e3) / GB, 2),
                    "hbm_GBps": round(dec_gbs, 1)},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": round(dom[1], 1), "peak": hbm,
-                     "peak_source": src, "unit": "GB/s", "frac": round(dom[1] / hbm, 4), "traffic": None,
+                     "peak_source": src, "unit": "GB/s", "frac": round(dom[1] / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom[2]},
         "torch_copy_GBps": round(copy_gbs, 1),
         "loopback_p2p": loop,
@@ -310,6 +311,19 @@ def run_loopback_p2p(uz, x, args):
             "bit_exact": bool(ok), "async_errors": errs,
             "wire_ratio": round(st["wire_bytes"] / max(1, st["raw_bytes"]), 5),
             "note": "sender+receiver kernels share one GPU (loopback), 1 GiB bf16 W"}
+
+
+def ncu_traffic(kernels, nbytes):
+    """DRAM bytes (read + write) per launch of the named kernels from the latest committed ncu
+    `--set full` capture (profiles/*_traffic.json, written by scripts/ncu_summary.py for the same
+    1 GiB bench command); None when absent or taken at another size."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files or nbytes != 1 << 30:
+        return None
+    d = json.load(open(files[-1]))
+    vals = [v for k, v in d.items() for name in kernels if name in k]
+    return int(sum(vals)) if vals else None
 
 
 def run_codec_e2e(uz, x, args, stream):

@@ -78,10 +78,18 @@ def main():
         for k, v in sorted(ours.items(), key=lambda kv: -kv[1]):
             lines.append(f"{k:40s} launches={cnt[k]:4d} mean={v / cnt[k] / 1e3:10.2f} us share={v / step:6.3f}")
         lines.append("")
+    traffic = {}
     for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep"))):
         v, u = raw(rep)
         if not v:
             continue
+        try:
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tb = sum(float(v[k].replace(",", "")) * scale.get(u.get(k, "byte"), 1)
+                     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            traffic[v.get("Kernel Name", rep).split("(")[0]] = int(tb)
+        except (KeyError, ValueError):
+            pass
         lines.append(f"## {os.path.basename(rep)}: {v.get('Kernel Name', '')[:90]}")
         for k in KEYS:
             if k in v:
@@ -96,6 +104,8 @@ def main():
         lines.append("  top stalls (warps per issue): " +
                      ", ".join(f"{n}={x:.2f}" for x, n in sorted(stalls, reverse=True)[:6]))
         lines.append("")
+    import json
+    json.dump(traffic, open(os.path.join(ROOT, "profiles", f"{tag}_traffic.json"), "w"), indent=1)
     out = os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt")
     open(out, "w").write("\n".join(lines) + "\n")
     print(out)

@@ -7,6 +7,4 @@ timeout 900 python bench.py > gpurun_out/bench_default.log 2> gpurun_out/bench_d
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1
 timeout 600 python __graft_entry__.py > gpurun_out/smoke.log 2>&1
 ./scripts/ncu_codec.sh
-ncu --set full --clock-control none --import-source on -k regex:k_table -s 1 -c 1 -o gpurun_out/prof_k_table -f \
-    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-loopback > /dev/null 2>&1
 cat gpurun_out/bench_default.log gpurun_out/bench_reference.log gpurun_out/smoke.log
