@@ -28,7 +28,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-BF16, F16, F32 = 0, 1, 2
+BF16, F16, F32, E4M3, E5M2 = 0, 1, 2, 3, 4
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED_DTYPE, ERR_CAPACITY, ERR_CORRUPT_STREAM, ERR_SIZE_MISMATCH = range(6)
 M = 4096
 L = 1 << 15
@@ -36,8 +36,10 @@ LANES = 32
 RAW_BLOCK = 0xFFFFFFFF
 HEADER_BYTES = 64
 
-ELEM_BYTES = {BF16: 2, F16: 2, F32: 4}
-NP_UINT = {BF16: np.uint16, F16: np.uint16, F32: np.uint32}
+ELEM_BYTES = {BF16: 2, F16: 2, F32: 4, E4M3: 1, E5M2: 1}
+NP_UINT = {BF16: np.uint16, F16: np.uint16, F32: np.uint32, E4M3: np.uint8, E5M2: np.uint8}
+GROUP_ELEMS = {BF16: 1, F16: 1, F32: 1, E4M3: 2, E5M2: 1}  # elements per symbol (P:485 e4m3 pairs)
+RES_BYTES = {BF16: 1, F16: 1, F32: 3, E4M3: 1, E5M2: 0}    # residual bytes per symbol
 
 
 def build(force: bool = False) -> str:
@@ -103,8 +105,11 @@ def as_bits(x: np.ndarray, dtype: int) -> np.ndarray:
 
 # ---------------------------------------------------------------- a1 split / join
 def split(dtype: int, bits: np.ndarray):
+    """Elements -> (symbols, residuals), one per symbol group (e4m3: pairs; len(bits) must be even)."""
     bits = np.ascontiguousarray(bits, dtype=NP_UINT[dtype])
-    n = bits.size
+    ge = GROUP_ELEMS[dtype]
+    assert bits.size % ge == 0
+    n = bits.size // ge
     sym = np.empty(n, np.uint8)
     res = np.empty(n, np.uint32)
     lib().uzo_split_array(dtype, _ptr(bits), n, _ptr(sym), _ptr(res))
@@ -114,7 +119,7 @@ def split(dtype: int, bits: np.ndarray):
 def join(dtype: int, sym: np.ndarray, res: np.ndarray) -> np.ndarray:
     sym = np.ascontiguousarray(sym, dtype=np.uint8)
     res = np.ascontiguousarray(res, dtype=np.uint32)
-    out = np.empty(sym.size, NP_UINT[dtype])
+    out = np.empty(sym.size * GROUP_ELEMS[dtype], NP_UINT[dtype])
     lib().uzo_join_array(dtype, _ptr(sym), _ptr(res), sym.size, _ptr(out))
     return out
 
@@ -210,7 +215,7 @@ def sections(stream: bytes) -> dict:
         off_tab = r16(off_res1 + ncoded)
     else:
         off_res1 = off_res0
-        off_tab = r16(off_res0 + ncoded)
+        off_tab = r16(off_res0 + RES_BYTES[hd["dtype"]] * ncoded)
     off_coff = off_tab + 512 * nc
     off_dir = r16(off_coff + 8 * nc)
     off_pay = r16(off_dir + 4 * nb)

@@ -30,7 +30,21 @@ size_t uzo_elem_bytes(int dtype) {
     case UZO_BF16: return 2;
     case UZO_F16: return 2;
     case UZO_F32: return 4;
+    case UZO_E4M3: return 1;
+    case UZO_E5M2: return 1;
     default: return 0;
+  }
+}
+
+/* two e4m3 values form one 16-bit unit whose two 4-bit exponent
+ * fields make one 8-bit symbol; every other dtype has one element per symbol. */
+size_t uzo_group_elems(int dtype) { return dtype == UZO_E4M3 ? 2 : 1; }
+size_t uzo_group_bytes(int dtype) { return uzo_elem_bytes(dtype) * uzo_group_elems(dtype); }
+size_t uzo_res_bytes(int dtype) {
+  switch (dtype) {
+    case UZO_F32: return 3;
+    case UZO_E5M2: return 0;
+    default: return uzo_elem_bytes(dtype) ? 1 : 0;
   }
 }
 
@@ -48,6 +62,17 @@ void uzo_split_elem(int dtype, uint32_t bits, uint8_t *sym, uint32_t *res) {
      * MSBs), the residual the low byte. */
     *sym = (uint8_t)((bits >> 8) & 0xFFu);
     *res = bits & 0xFFu;
+  } else if (dtype == UZO_E4M3) {
+    /* e4m3 (s:7 e:6..3 m:2..0), pair (a, b): symbol = exp_a<<4 | exp_b,
+     * residual = s_a<<7 | m_a<<4 | s_b<<3 | m_b */
+    uint32_t a = bits & 0xFFu, b = (bits >> 8) & 0xFFu;
+    uint32_t ea = (a >> 3) & 0xFu, eb = (b >> 3) & 0xFu;
+    *sym = (uint8_t)((ea << 4) | eb);
+    *res = ((a >> 7) << 7) | ((a & 7u) << 4) | ((b >> 7) << 3) | (b & 7u);
+  } else if (dtype == UZO_E5M2) {
+    /* SPEC S:33, S:94 (R24): the whole byte is the symbol, no residual */
+    *sym = (uint8_t)(bits & 0xFFu);
+    *res = 0;
   } else { /* UZO_F32 */
     uint32_t sign = (bits >> 31) & 1u;
     uint32_t expo = (bits >> 23) & 0xFFu;
@@ -66,6 +91,13 @@ uint32_t uzo_join_elem(int dtype, uint8_t sym, uint32_t res) {
     return (sign << 15) | ((uint32_t)sym << 7) | frac;
   } else if (dtype == UZO_F16) {
     return ((uint32_t)sym << 8) | (res & 0xFFu);
+  } else if (dtype == UZO_E4M3) {
+    uint32_t ea = (uint32_t)sym >> 4, eb = (uint32_t)sym & 0xFu;
+    uint32_t a = (((res >> 7) & 1u) << 7) | (ea << 3) | ((res >> 4) & 7u);
+    uint32_t b = (((res >> 3) & 1u) << 7) | (eb << 3) | (res & 7u);
+    return a | (b << 8);
+  } else if (dtype == UZO_E5M2) {
+    return sym;
   } else {
     uint32_t lo16 = res & 0xFFFFu;
     uint32_t hi8 = (res >> 16) & 0xFFu;
@@ -75,21 +107,22 @@ uint32_t uzo_join_elem(int dtype, uint8_t sym, uint32_t res) {
   }
 }
 
+/* n = number of symbol groups (elements for every dtype but e4m3: pairs). */
 void uzo_split_array(int dtype, const void *in, size_t n, uint8_t *sym, uint32_t *res) {
   const uint8_t *b = (const uint8_t *)in;
+  size_t w = uzo_group_bytes(dtype);
   for (size_t i = 0; i < n; ++i) {
-    uint32_t bits = dtype == UZO_F32 ? (uint32_t)b[4 * i] | ((uint32_t)b[4 * i + 1] << 8) |
-                                           ((uint32_t)b[4 * i + 2] << 16) | ((uint32_t)b[4 * i + 3] << 24)
-                                     : (uint32_t)b[2 * i] | ((uint32_t)b[2 * i + 1] << 8);
+    uint32_t bits = 0;
+    for (size_t k = 0; k < w; ++k) bits |= (uint32_t)b[w * i + k] << (8 * k);
     uzo_split_elem(dtype, bits, &sym[i], &res[i]);
   }
 }
 
 void uzo_join_array(int dtype, const uint8_t *sym, const uint32_t *res, size_t n, void *out) {
   uint8_t *b = (uint8_t *)out;
+  size_t w = uzo_group_bytes(dtype);
   for (size_t i = 0; i < n; ++i) {
     uint32_t v = uzo_join_elem(dtype, sym[i], res[i]);
-    size_t w = dtype == UZO_F32 ? 4 : 2;
     for (size_t k = 0; k < w; ++k) b[w * i + k] = (uint8_t)(v >> (8 * k));
   }
 }
@@ -225,7 +258,7 @@ static size_t round16(size_t v) { return (v + 15u) & ~(size_t)15u; }
 
 static void resolve_params(int dtype, const uzo_params *p, uint32_t *B, uint32_t *CB,
                            uint32_t *S, int *global) {
-  size_t eb = uzo_elem_bytes(dtype);
+  size_t eb = uzo_group_bytes(dtype); /* input bytes per symbol */
   *B = (p && p->block_symbols) ? p->block_symbols : 4096u;
   *global = (p && p->global_table) ? 1 : 0;
   *CB = (p && p->chunk_blocks) ? p->chunk_blocks : (uint32_t)((8u << 20) / (*B * eb));
@@ -233,12 +266,15 @@ static void resolve_params(int dtype, const uzo_params *p, uint32_t *B, uint32_t
   *S = (p && p->sample_symbols) ? p->sample_symbols : (uint32_t)((256u << 10) / eb);
 }
 
+/* n counts ELEMENTS; blocks count symbol groups (n_coded groups are coded,
+ * the remaining n - n_coded * group_elems elements form the raw tail). */
 static void make_layout(int dtype, size_t n, uint32_t B, uint32_t CB, uint32_t S, int global,
                         size_t payload_bytes, layout_t *L) {
   size_t eb = uzo_elem_bytes(dtype);
+  size_t ge = uzo_group_elems(dtype);
   L->B = B;
   L->n = n;
-  L->n_blocks = n / B;
+  L->n_blocks = (n / ge) / B;
   L->n_coded = L->n_blocks * B;
   L->global = global;
   if (global) {
@@ -255,14 +291,14 @@ static void make_layout(int dtype, size_t n, uint32_t B, uint32_t CB, uint32_t S
     L->off_tab = round16(L->off_res1 + L->n_coded);
   } else {
     L->off_res1 = L->off_res0;
-    L->off_tab = round16(L->off_res0 + L->n_coded);
+    L->off_tab = round16(L->off_res0 + uzo_res_bytes(dtype) * L->n_coded);
   }
   L->off_coff = L->off_tab + 512 * L->n_chunks;
   L->off_dir = round16(L->off_coff + 8 * L->n_chunks);
   L->off_pay = round16(L->off_dir + 4 * L->n_blocks);
   L->payload_bytes = payload_bytes;
   L->off_tail = round16(L->off_pay + payload_bytes);
-  L->total = L->off_tail + (n - L->n_coded) * eb;
+  L->total = L->off_tail + (n - L->n_coded * ge) * eb;
 }
 
 static void put16(uint8_t *p, uint32_t v) { p[0] = (uint8_t)v; p[1] = (uint8_t)(v >> 8); }
@@ -286,10 +322,12 @@ static uint64_t get64(const uint8_t *p) {
 
 static uint32_t load_elem(int dtype, const uint8_t *in, size_t i) {
   if (dtype == UZO_F32) return get32(in + 4 * i);
-  return get16(in + 2 * i);
+  if (dtype == UZO_E5M2) return in[i];
+  return get16(in + 2 * i); /* bf16, f16, and an e4m3 pair */
 }
 static void store_elem(int dtype, uint8_t *out, size_t i, uint32_t v) {
   if (dtype == UZO_F32) put32(out + 4 * i, v);
+  else if (dtype == UZO_E5M2) out[i] = (uint8_t)v;
   else put16(out + 2 * i, v);
 }
 
@@ -300,7 +338,7 @@ size_t uzo_compress_bound(size_t n, int dtype, const uzo_params *p) {
   if (uzo_elem_bytes(dtype) == 0) return 0;
   resolve_params(dtype, p, &B, &CB, &S, &global);
   layout_t L;
-  make_layout(dtype, n, B, CB, S, global, (n / B) * (size_t)B, &L);
+  make_layout(dtype, n, B, CB, S, global, ((n / uzo_group_elems(dtype)) / B) * (size_t)B, &L);
   return L.total;
 }
 
@@ -387,7 +425,7 @@ int uzo_compress(int dtype, const void *in_v, size_t n, const uzo_params *p, uin
     if (dtype == UZO_F32) {
       put16(out + L.off_res0 + 2 * i, res[i] & 0xFFFFu);
       out[L.off_res1 + i] = (uint8_t)(res[i] >> 16);
-    } else {
+    } else if (uzo_res_bytes(dtype) == 1) {
       out[L.off_res0 + i] = (uint8_t)res[i];
     }
   }
@@ -411,7 +449,7 @@ int uzo_compress(int dtype, const void *in_v, size_t n, const uzo_params *p, uin
     }
   }
   /* raw tail */
-  memcpy(out + L.off_tail, in + L.n_coded * eb, (n - L.n_coded) * eb);
+  memcpy(out + L.off_tail, in + L.n_coded * uzo_group_bytes(dtype), (n - L.n_coded * uzo_group_elems(dtype)) * eb);
   *out_bytes = L.total;
 
 done:
@@ -489,15 +527,19 @@ int uzo_decompress(const uint8_t *in, size_t in_bytes, void *out_v, size_t n, in
         uint32_t r;
         if (dtype == UZO_F32)
           r = get16(in + L.off_res0 + 2 * e) | ((uint32_t)in[L.off_res1 + e] << 16);
-        else
+        else if (uzo_res_bytes(dtype) == 1)
           r = in[L.off_res0 + e];
+        else
+          r = 0;
         store_elem(dtype, out, e, uzo_join_elem(dtype, sym[i], r));
       }
       run += size;
     }
   }
   if (status == UZO_OK && run != L.payload_bytes) status = UZO_ERR_CORRUPT_STREAM;
-  if (status == UZO_OK) memcpy(out + L.n_coded * eb, in + L.off_tail, (n - L.n_coded) * eb);
+  if (status == UZO_OK)
+    memcpy(out + L.n_coded * uzo_group_bytes(dtype), in + L.off_tail,
+           (n - L.n_coded * uzo_group_elems(dtype)) * eb);
   free(words);
   free(sym);
   return status;

@@ -31,7 +31,7 @@ extern "C" {
 #endif
 
 /* dtype codes (same numbering as include/uzip.h, restated, not shared) */
-enum { UZO_BF16 = 0, UZO_F16 = 1, UZO_F32 = 2 };
+enum { UZO_BF16 = 0, UZO_F16 = 1, UZO_F32 = 2, UZO_E4M3 = 3, UZO_E5M2 = 4 };
 
 /* status codes (same numbering as include/uzip.h, restated, not shared) */
 enum {
@@ -60,11 +60,20 @@ typedef struct {
 } uzo_params;
 
 size_t uzo_elem_bytes(int dtype);
+/* A symbol group is the unit that yields one 8-bit symbol: one element for
+ * bf16/f16/f32/e5m2, a pair of elements for e4m3 ("pack two FP8 values
+ * into a single 16-bit unit").  group bytes = elem bytes * elems. */
+size_t uzo_group_elems(int dtype);
+size_t uzo_group_bytes(int dtype);
+/* residual bytes per group: 1 (bf16, f16, e4m3), 3 (f32: lo16 + hi8 planes), 0 (e5m2) */
+size_t uzo_res_bytes(int dtype);
 
-/* a1 Split: one element -> (symbol, residual).
- * bits holds the element's raw bits (16 or 32 of them).  For f32 the
- * residual is 24 bits: lo16 (bits 15..0) | hi8 << 16 where
- * hi8 = sign<<7 | bits 22..16.  For bf16/f16 the residual is one byte. */
+/* a1 Split: one symbol group -> (symbol, residual).
+ * bits holds the group's raw bits, little-endian (16 or 32 of them; for e4m3
+ * the pair (a, b) = (bits & 0xFF, bits >> 8); for e5m2 the one byte).  For
+ * f32 the residual is 24 bits: lo16 (bits 15..0) | hi8 << 16 where
+ * hi8 = sign<<7 | bits 22..16.  For bf16/f16/e4m3 the residual is one byte,
+ * for e5m2 it is empty (0). */
 void uzo_split_elem(int dtype, uint32_t bits, uint8_t *sym, uint32_t *res);
 uint32_t uzo_join_elem(int dtype, uint8_t sym, uint32_t res);
 void uzo_split_array(int dtype, const void *in, size_t n, uint8_t *sym, uint32_t *res);

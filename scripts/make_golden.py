@@ -29,6 +29,8 @@ CASES = [
      {"block_symbols": 1024, "chunk_blocks": 4, "sample_symbols": 2000}),
     ("bf16_w_chunks8", oracle.BF16, lambda: synth.weights(20 * 1024 + 7, 1006),
      {"block_symbols": 1024, "chunk_blocks": 8, "sample_symbols": 3000}),
+    ("e4m3_u_2blk_odd", oracle.E4M3, lambda: synth.uniform(2 * 8192 + 5, 1007, oracle.E4M3), {}),
+    ("e5m2_w_3blk_tail", oracle.E5M2, lambda: synth.weights(3 * 4096 + 9, 1008, oracle.E5M2), {}),
 ]
 
 

@@ -21,9 +21,10 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-BF16, F16, F32 = 0, 1, 2
-_TORCH = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32}
-_UINT = {BF16: np.uint16, F16: np.uint16, F32: np.uint32}
+BF16, F16, F32, E4M3, E5M2 = 0, 1, 2, 3, 4
+_TORCH = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32, E4M3: torch.float8_e4m3fn,
+          E5M2: torch.float8_e5m2}
+_UINT = {BF16: np.uint16, F16: np.uint16, F32: np.uint32, E4M3: np.uint8, E5M2: np.uint8}
 
 
 def _gen(seed: int) -> torch.Generator:
@@ -36,6 +37,8 @@ def _bits(t: torch.Tensor, dtype: int) -> np.ndarray:
     t = t.to(_TORCH[dtype]).contiguous()
     if dtype == F32:
         return t.view(torch.int32).numpy().view(np.uint32).reshape(-1).copy()
+    if dtype in (E4M3, E5M2):
+        return t.view(torch.uint8).numpy().reshape(-1).copy()
     return t.view(torch.int16).numpy().view(np.uint16).reshape(-1).copy()
 
 
@@ -78,7 +81,7 @@ def gradients(n: int, seed: int) -> np.ndarray:
 
 def random_bits(n: int, seed: int, dtype: int = BF16) -> np.ndarray:
     rng = np.random.default_rng(seed)
-    hi = 1 << (32 if dtype == F32 else 16)
+    hi = 1 << (32 if dtype == F32 else (8 if dtype in (E4M3, E5M2) else 16))
     return rng.integers(0, hi, size=n, dtype=np.uint64).astype(_UINT[dtype])
 
 
@@ -92,6 +95,8 @@ def special_mix(n: int, seed: int, dtype: int = BF16) -> np.ndarray:
     elif dtype == BF16:
         pool = np.array([0x0000, 0x8000, 0x7F80, 0xFF80, 0x7FC0, 0x7F81, 0xFFFF, 0x0001, 0x807F,
                          0x3F80, 0xBF80, 0x7F7F], np.uint16)
+    elif dtype in (E4M3, E5M2):  # zeros, NaN (e4m3fn 0x7F/0xFF), e5m2 +-inf 0x7C/0xFC, denormals, max
+        pool = np.array([0x00, 0x80, 0x7F, 0xFF, 0x7C, 0xFC, 0x01, 0x81, 0x7E, 0x38, 0x7B, 0xFB], np.uint8)
     else:
         pool = np.array([0x0000, 0x8000, 0x7C00, 0xFC00, 0x7E00, 0x7C01, 0xFFFF, 0x0001, 0x83FF,
                          0x3C00, 0xBC00, 0x7BFF], np.uint16)
