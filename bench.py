@@ -250,6 +250,7 @@ def run_codec(args):
     if not args.no_e2e:
         e2e = run_codec_e2e(uz, x, args, stream)
     loop = None if args.no_loopback else run_loopback_p2p(uz, x, args)
+    per_dtype = run_per_dtype(uz, args)
 
     line = {
         "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",
@@ -266,6 +267,7 @@ def run_codec(args):
                      "algorithmic_bytes_per_launch": dom[2]},
         "torch_copy_GBps": round(copy_gbs, 1),
         "loopback_p2p": loop,
+        "per_dtype_uniform": per_dtype,
         "clocks": clk.summary(),
         "gpu_launches": 3 * args.steps,
     }
@@ -274,6 +276,43 @@ def run_codec(args):
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
+
+
+def run_per_dtype(uz, args):
+    """Context (the paper's per-dtype table): ratio and round-trip GB/s of 256 MiB of
+    U[-1,1] (the paper's synthetic input) per dtype; paper ratios f16 0.83, f32 0.82,
+    bf16 0.64, e4m3 0.77, e5m2 0.70."""
+    import torch
+    out = {}
+    nbytes = 256 << 20
+    g = torch.Generator(device="cuda")
+    for name, tdt, paper in (("bf16", torch.bfloat16, 0.64), ("f16", torch.float16, 0.83),
+                             ("f32", torch.float32, 0.82), ("e4m3", torch.float8_e4m3fn, 0.77),
+                             ("e5m2", torch.float8_e5m2, 0.70)):
+        g.manual_seed(7)
+        n = nbytes // torch.tensor([], dtype=tdt).element_size()
+        x = (torch.rand(n, device="cuda", generator=g) * 2 - 1).to(tdt)
+        dt = uz.uz_dtype(tdt)
+        cap = uz.compress_bound(n, dt)
+        buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+        y = torch.empty_like(x)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ws = uz.Workspace(0).get(uz.workspace_bytes(n, dt))
+        for _ in range(2):
+            uz.compress(x, out=buf, out_bytes=nb, ws=ws)
+            uz.decompress(buf, n, dt, out=y, status=st, ws=ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            uz.compress(x, out=buf, out_bytes=nb, ws=ws)
+            uz.decompress(buf, n, dt, out=y, status=st, ws=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        ok = int(st.item()) == 0 and torch.equal(x.view(torch.uint8), y.view(torch.uint8))
+        out[name] = {"ratio": round(int(nb.item()) / nbytes, 4), "paper_ratio": paper,
+                     "roundtrip_GBps": round(nbytes / (e0.elapsed_time(e1) / 5 / 1e3) / GB, 1), "bit_exact": ok}
+    return out
 
 
 def run_loopback_p2p(uz, x, args):

@@ -40,8 +40,9 @@
 extern "C" {
 #endif
 
-/* Element types the codec splits (fp8 is not in this build). */
-typedef enum { UZIP_BF16 = 0, UZIP_F16 = 1, UZIP_F32 = 2 } uzip_dtype_t;
+/* Element types the codec splits.  fp8: e4m3 pairs form one symbol (R23), e5m2
+ * bytes are symbols (R24); fp8 is not reduced (reduce-scatter / allreduce, R22). */
+typedef enum { UZIP_BF16 = 0, UZIP_F16 = 1, UZIP_F32 = 2, UZIP_E4M3 = 3, UZIP_E5M2 = 4 } uzip_dtype_t;
 
 /* Reduction operators (P:402 names sum, min, max; this build: sum, R11). */
 typedef enum { UZIP_SUM = 0 } uzip_op_t;

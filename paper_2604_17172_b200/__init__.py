@@ -22,16 +22,17 @@ from . import _build
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("UZIP_LIB_PATH") or os.path.join(_HERE, "libuzip.so")  # override: tuning variants
 
-BF16, F16, F32 = 0, 1, 2
+BF16, F16, F32, E4M3, E5M2 = 0, 1, 2, 3, 4
 SUM = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED_DTYPE", 3: "CAPACITY", 4: "CORRUPT_STREAM",
           5: "SIZE_MISMATCH", 6: "CUDA", 7: "COMM", 8: "TIMEOUT", 9: "NOT_IMPLEMENTED"}
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED_DTYPE, ERR_CAPACITY, ERR_CORRUPT_STREAM, ERR_SIZE_MISMATCH, \
     ERR_CUDA, ERR_COMM, ERR_TIMEOUT, ERR_NOT_IMPLEMENTED = range(10)
 
-_TORCH_TO_UZ = {torch.bfloat16: BF16, torch.float16: F16, torch.float32: F32}
+_TORCH_TO_UZ = {torch.bfloat16: BF16, torch.float16: F16, torch.float32: F32, torch.float8_e4m3fn: E4M3,
+                torch.float8_e5m2: E5M2}
 _UZ_TO_TORCH = {v: k for k, v in _TORCH_TO_UZ.items()}
-ELEM_BYTES = {BF16: 2, F16: 2, F32: 4}
+ELEM_BYTES = {BF16: 2, F16: 2, F32: 4, E4M3: 1, E5M2: 1}
 
 EXPORTED = [
     "uzip_compress_bound", "uzip_workspace_bytes", "uzip_workspace_init", "uzip_compress", "uzip_decompress",

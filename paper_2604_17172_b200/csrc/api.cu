@@ -12,8 +12,8 @@ using namespace uzip;
 namespace uzip {
 
 uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g) {
-  if (dtype < 0 || dtype > 2) return UZIP_ERR_UNSUPPORTED_DTYPE;
-  const uint32_t eb = elem_bytes(dtype);
+  if (dtype < 0 || dtype >= kNumDtypes) return UZIP_ERR_UNSUPPORTED_DTYPE;
+  const uint32_t eb = group_bytes(dtype);  // input bytes per symbol
   uint32_t B = (p && p->block_symbols) ? p->block_symbols : 4096u;
   if (!(B == 1024 || B == 2048 || B == 4096)) return UZIP_ERR_INVALID_ARG;
   const bool global = p && p->global_table;
@@ -105,7 +105,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
 
 uzip_status_t uzip_decompress(const void *in, size_t in_bytes, void *out, size_t count, uzip_dtype_t dtype,
                               int32_t *d_status, void *ws, size_t ws_bytes, void *stream) {
-  if ((int)dtype < 0 || (int)dtype > 2) return UZIP_ERR_UNSUPPORTED_DTYPE;
+  if ((int)dtype < 0 || (int)dtype >= kNumDtypes) return UZIP_ERR_UNSUPPORTED_DTYPE;
   if (!in || !ws || !d_status || !aligned16(in) || !aligned16(ws)) return UZIP_ERR_INVALID_ARG;
   if (count > 0 && (!out || !aligned16(out))) return UZIP_ERR_INVALID_ARG;
   if (ws_bytes < 64) return UZIP_ERR_CAPACITY;

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(256, 4) k_decode(const uint8_t *__restrict__ i
     }
     // raw tail
     if (blockIdx.x == 0) {
-      const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+      const uint64_t tail_bytes = g.tail_bytes();
       const uint8_t *src = in + g.off_tail(payload);
       uint8_t *dst = out + g.n_coded * g.eb;
       for (uint64_t i = tid; i < tail_bytes; i += 256) dst[i] = src[i];
@@ -299,6 +299,8 @@ cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void
   switch (dtype) {
     case kBF16: return launch_decode_t<kBF16>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
     case kF16: return launch_decode_t<kF16>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
+    case kE4M3: return launch_decode_t<kE4M3>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
+    case kE5M2: return launch_decode_t<kE5M2>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
     default: return launch_decode_t<kF32>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
   }
 }

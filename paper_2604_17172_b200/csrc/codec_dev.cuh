@@ -93,6 +93,10 @@ __device__ __forceinline__ void join_block(const uint8_t *syms, const uint8_t *s
       const uint32_t h4 = ld_cg_u32c(stream + g.off_res1 + b * B + e);
       st_any16(dst + 4 * e, join4_f32(s4, lo, h4));
     }
+  } else if (DT == kE5M2) {  // the symbols are the bytes (R24)
+#pragma unroll 4
+    for (uint32_t e = lane * 16; e < (uint32_t)B; e += 512)
+      st_any16(dst + e, *reinterpret_cast<const uint4 *>(syms + e));
   } else {
 #pragma unroll 4
     for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
@@ -102,49 +106,12 @@ __device__ __forceinline__ void join_block(const uint8_t *syms, const uint8_t *s
       if (DT == kBF16) {
         join4_bf16(s8.x, r8.x, o.x, o.y);
         join4_bf16(s8.y, r8.y, o.z, o.w);
+      } else if (DT == kE4M3) {
+        join4_e4m3(s8.x, r8.x, o.x, o.y);
+        join4_e4m3(s8.y, r8.y, o.z, o.w);
       } else {
         join4_f16(s8.x, r8.x, o.x, o.y);
         join4_f16(s8.y, r8.y, o.z, o.w);
-      }
-      st_any16(dst + 2 * e, o);
-    }
-  }
-}
-
-// Residual plane of one block held in registers (16-bit types): issued before
-// the rANS rounds so its latency hides behind them.  fp32 reads at join time.
-template <int DT, int B>
-struct ResidualRegs {
-  static constexpr int kN = (DT == kF32) ? 1 : B / 256;  // uint2 (8 residual bytes) per lane step
-  uint2 r[kN];
-  __device__ __forceinline__ void load(const uint8_t *stream, const StreamGeom &g, uint64_t b) {
-    if (DT != kF32) {
-      const int lane = threadIdx.x & 31;
-#pragma unroll
-      for (int i = 0; i < kN; ++i) r[i] = ld_cg_v2(stream + g.off_res0 + b * B + lane * 8 + 256 * i);
-    }
-  }
-};
-
-template <int DT, int B>
-__device__ __forceinline__ void join_block_regs(const uint8_t *syms, const ResidualRegs<DT, B> &R,
-                                                const uint8_t *stream, const StreamGeom &g, uint64_t b,
-                                                uint8_t *dst) {
-  if (DT == kF32) {
-    join_block<DT, B>(syms, stream, g, b, dst);
-  } else {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int i = 0; i < ResidualRegs<DT, B>::kN; ++i) {
-      const uint32_t e = lane * 8 + 256 * i;
-      const uint2 s8 = *reinterpret_cast<const uint2 *>(syms + e);
-      uint4 o;
-      if (DT == kBF16) {
-        join4_bf16(s8.x, R.r[i].x, o.x, o.y);
-        join4_bf16(s8.y, R.r[i].y, o.z, o.w);
-      } else {
-        join4_f16(s8.x, R.r[i].x, o.x, o.y);
-        join4_f16(s8.y, R.r[i].y, o.z, o.w);
       }
       st_any16(dst + 2 * e, o);
     }
@@ -166,8 +133,10 @@ struct StoreEpi {
     if (DT == kF32) {
       st_any16(dst + 4 * e0, a);
       st_any16(dst + 4 * e0 + 16, b);
+    } else if (DT == kE5M2) {
+      st_any8(dst + e0, make_uint2(a.x, a.y));  // 8 symbols = 8 output bytes
     } else {
-      st_any16(dst + 2 * e0, a);
+      st_any16(dst + 2 * e0, a);  // e0 counts groups: 2 bytes each (bf16, f16, e4m3 pair)
     }
   }
 };
@@ -184,14 +153,14 @@ __device__ __forceinline__ bool decode_join_warp_epi(const uint8_t *pay, uint32_
   const uint16_t *pay16 = reinterpret_cast<const uint16_t *>(pay) + 64;
   const uint8_t *res0 = stream + g.off_res0 + (DT == kF32 ? 2 : 1) * (b * B) + (DT == kF32 ? 16 : 8) * lane;
   const uint8_t *res1 = stream + g.off_res1 + b * B + 8 * lane;  // fp32 hi8 plane
-  uint4 rlo[kPF];   // fp32: lo16 of 8 elements; 16-bit types: .x/.y = 8 residual bytes
+  uint4 rlo[kPF];   // fp32: lo16 of 8 elements; bf16/f16/e4m3: .x/.y = 8 residual bytes; e5m2: none
   uint2 rhi[kPF];   // fp32: hi8 of 8 elements
 #pragma unroll
   for (int i = 0; i < kPF; ++i) {
     if (DT == kF32) {
       rlo[i] = ld_cg_v4(res0 + 512 * i);
       rhi[i] = ld_cg_v2(res1 + 256 * i);
-    } else {
+    } else if (DT != kE5M2) {
       const uint2 v = ld_cg_v2(res0 + 256 * i);
       rlo[i] = make_uint4(v.x, v.y, 0, 0);
     }
@@ -223,18 +192,24 @@ __device__ __forceinline__ bool decode_join_warp_epi(const uint8_t *pay, uint32_
       if (DT == kF32) {
         epi.template apply<DT>(e0, join4_f32(s8.x, make_uint2(rlo[q].x, rlo[q].y), rhi[q].x),
                                join4_f32(s8.y, make_uint2(rlo[q].z, rlo[q].w), rhi[q].y));
+      } else if (DT == kE5M2) {
+        const uint4 v = make_uint4(s8.x, s8.y, 0, 0);
+        epi.template apply<DT>(e0, v, v);
       } else {
         uint4 v;
         if (DT == kBF16) {
           join4_bf16(s8.x, rlo[q].x, v.x, v.y);
           join4_bf16(s8.y, rlo[q].y, v.z, v.w);
+        } else if (DT == kE4M3) {
+          join4_e4m3(s8.x, rlo[q].x, v.x, v.y);
+          join4_e4m3(s8.y, rlo[q].y, v.z, v.w);
         } else {
           join4_f16(s8.x, rlo[q].x, v.x, v.y);
           join4_f16(s8.y, rlo[q].y, v.z, v.w);
         }
         epi.template apply<DT>(e0, v, v);
       }
-      if (gi + kPF < kGroups) {
+      if (gi + kPF < kGroups && DT != kE5M2) {
         if (DT == kF32) {
           rlo[q] = ld_cg_v4(res0 + 512 * (gi + kPF));
           rhi[q] = ld_cg_v2(res1 + 256 * (gi + kPF));

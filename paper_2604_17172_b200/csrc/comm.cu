@@ -155,8 +155,9 @@ uint64_t round_elems(uzip_comm *c, int dt, bool compressed, uint64_t count, Stre
            t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_blocks) <= c->ws_job_bytes;
   };
   // whole table chunks when one fits a slot, else whole tiles (a round shorter than a chunk has one chunk)
-  uint64_t unit = g.global ? (uint64_t)g.B * kTileBlocks : (uint64_t)g.CB * g.B;
-  if (!fits(unit)) unit = (uint64_t)g.B * kTileBlocks;
+  const uint64_t ge = group_elems(dt);  // rounds split at symbol-group boundaries
+  uint64_t unit = (g.global ? (uint64_t)g.B * kTileBlocks : (uint64_t)g.CB * g.B) * ge;
+  if (!fits(unit)) unit = (uint64_t)g.B * kTileBlocks * ge;
   uint64_t lo = 1, hi = cap / unit + 1;
   while (lo < hi) {  // largest k with k*unit fitting a slot and the workspace
     const uint64_t k = (lo + hi + 1) / 2;
@@ -288,7 +289,11 @@ uzip_status_t begin_call(uzip_comm *c, uint64_t egress_raw, bool compressed, cud
 }
 
 uzip_status_t check_dtype(uzip_dtype_t dt) {
-  return ((int)dt < 0 || (int)dt > 2) ? UZIP_ERR_UNSUPPORTED_DTYPE : UZIP_OK;
+  return ((int)dt < 0 || (int)dt >= kNumDtypes) ? UZIP_ERR_UNSUPPORTED_DTYPE : UZIP_OK;
+}
+// reductions are defined for bf16/f16/f32 only (R22)
+uzip_status_t check_reduce_dtype(uzip_dtype_t dt) {
+  return ((int)dt < 0 || (int)dt > kF32) ? UZIP_ERR_UNSUPPORTED_DTYPE : UZIP_OK;
 }
 
 }  // namespace
@@ -478,7 +483,7 @@ uzip_status_t uzip_allgather(const void *sendbuf, void *recvbuf, size_t sendcoun
 uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t recvcount, uzip_dtype_t dtype,
                                   uzip_op_t op, uzip_comm_t c, void *stream) {
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
-  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
   if (op != UZIP_SUM) return UZIP_ERR_INVALID_ARG;
   if (recvcount == 0) return UZIP_OK;
   if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
@@ -522,7 +527,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
 uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype, uzip_op_t op,
                              uzip_comm_t c, void *stream) {
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
-  if (uzip_status_t s = check_dtype(dtype)) return s;
+  if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
   if (op != UZIP_SUM) return UZIP_ERR_INVALID_ARG;
   if (count == 0) return UZIP_OK;
   const int N = c->nranks;
@@ -628,7 +633,7 @@ uzip_status_t uzip_broadcast(void *buf, size_t count, uzip_dtype_t dtype, int ro
   // forwards the compressed bytes to the other receivers; every receiver decodes every piece.
   const int R = N - 1;
   uint64_t P = (count + R - 1) / R;
-  P = (P + 7) & ~7ull;  // 16-byte aligned pieces
+  P = (P + 15) & ~15ull;  // pieces of 16 elements: 16-byte aligned for every dtype
   auto piece_len = [&](int k) -> uint64_t {
     const uint64_t lo = std::min<uint64_t>(count, (uint64_t)k * P), hi = std::min<uint64_t>(count, lo + P);
     return hi - lo;

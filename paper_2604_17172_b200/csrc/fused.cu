@@ -8,8 +8,11 @@ namespace uzip {
 cudaError_t launch_tables_bf16(const Plan &, cudaStream_t);
 cudaError_t launch_tables_f16(const Plan &, cudaStream_t);
 cudaError_t launch_tables_f32(const Plan &, cudaStream_t);
+cudaError_t launch_tables_e4m3(const Plan &, cudaStream_t);
+cudaError_t launch_tables_e5m2(const Plan &, cudaStream_t);
 #define UZIP_DECL(n) cudaError_t launch_fused_##n(const Plan &, uint32_t, cudaStream_t, int);
 UZIP_DECL(bf16_enc) UZIP_DECL(bf16_red) UZIP_DECL(f16_enc) UZIP_DECL(f16_red) UZIP_DECL(f32_enc) UZIP_DECL(f32_red)
+UZIP_DECL(e4m3_enc) UZIP_DECL(e5m2_enc)
 #undef UZIP_DECL
 cudaError_t preload_bf16_enc();
 cudaError_t preload_bf16_red();
@@ -17,10 +20,12 @@ cudaError_t preload_f16_enc();
 cudaError_t preload_f16_red();
 cudaError_t preload_f32_enc();
 cudaError_t preload_f32_red();
+cudaError_t preload_e4m3_enc();
+cudaError_t preload_e5m2_enc();
 
 cudaError_t preload_kernels() {
-  cudaError_t (*fns[])() = {preload_bf16_enc, preload_bf16_red, preload_f16_enc,
-                            preload_f16_red,  preload_f32_enc,  preload_f32_red};
+  cudaError_t (*fns[])() = {preload_bf16_enc, preload_bf16_red, preload_f16_enc, preload_f16_red,
+                            preload_f32_enc,  preload_f32_red,  preload_e4m3_enc, preload_e5m2_enc};
   for (auto f : fns) {
     const cudaError_t e = f();
     if (e != cudaSuccess) return e;
@@ -33,6 +38,8 @@ cudaError_t launch_tables(int dtype, const Plan &p, cudaStream_t st) {
   switch (dtype) {
     case kBF16: return launch_tables_bf16(p, st);
     case kF16: return launch_tables_f16(p, st);
+    case kE4M3: return launch_tables_e4m3(p, st);
+    case kE5M2: return launch_tables_e5m2(p, st);
     default: return launch_tables_f32(p, st);
   }
 }
@@ -49,6 +56,8 @@ cudaError_t launch_fused(int dtype, const Plan &p, cudaStream_t st, int max_ctas
   switch (dtype) {
     case kBF16: return red ? launch_fused_bf16_red(p, B, st, max_ctas) : launch_fused_bf16_enc(p, B, st, max_ctas);
     case kF16: return red ? launch_fused_f16_red(p, B, st, max_ctas) : launch_fused_f16_enc(p, B, st, max_ctas);
+    case kE4M3: return red ? cudaErrorNotSupported : launch_fused_e4m3_enc(p, B, st, max_ctas);
+    case kE5M2: return red ? cudaErrorNotSupported : launch_fused_e5m2_enc(p, B, st, max_ctas);
     default: return red ? launch_fused_f32_red(p, B, st, max_ctas) : launch_fused_f32_enc(p, B, st, max_ctas);
   }
 }

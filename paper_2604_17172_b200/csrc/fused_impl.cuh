@@ -70,9 +70,9 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
   for (int i = tid; i < kHistWarps * 256; i += kHistThreads) (&hist[0][0])[i] = 0;
   __syncthreads();
 
-  constexpr uint32_t kPer = (DT == kF32) ? 4 : 8;  // symbols per 16-byte vector
+  constexpr uint32_t kPer = VecTraits<DT>::kSym;  // symbols per 16-byte vector
   constexpr int kUnroll = 8;
-  const uint8_t *base = J.in + (uint64_t)c * g.CB * g.B * elem_bytes(DT);
+  const uint8_t *base = J.in + (uint64_t)c * g.CB * g.B * group_bytes(DT);
   const uint32_t nvec = len / kPer;
   const uint32_t per = (nvec + parts - 1) / parts;
   const uint32_t v_lo = part * per, v_hi = min(nvec, v_lo + per);
@@ -86,24 +86,12 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const bool ok = v0 + u * kHistThreads + tid < v_hi;
-      uint32_t s_lo, s_hi = 0;
-      if (DT == kBF16) {
-        uint32_t r;
-        split4_bf16(w[u].x, w[u].y, s_lo, r);
-        split4_bf16(w[u].z, w[u].w, s_hi, r);
-      } else if (DT == kF16) {
-        uint32_t r;
-        split4_f16(w[u].x, w[u].y, s_lo, r);
-        split4_f16(w[u].z, w[u].w, s_hi, r);
-      } else {
-        uint2 lo;
-        uint32_t hi;
-        split4_f32(w[u], s_lo, lo, hi);
-      }
+      uint32_t sw[4];
+      vec_symbols<DT>(w[u], sw);
       // warp-aggregated increments: the lanes holding the same symbol add once
 #pragma unroll
       for (int k = 0; k < (int)kPer; ++k) {
-        const uint32_t sy = ok ? ((k < 4 ? s_lo : s_hi) >> (8 * (k & 3))) & 0xFFu : 0x100u;
+        const uint32_t sy = ok ? (sw[k >> 2] >> (8 * (k & 3))) & 0xFFu : 0x100u;
         const uint32_t peers = __match_any_sync(0xFFFFFFFFu, sy);
         if (sy < 256 && (uint32_t)lane == (uint32_t)(__ffs(peers) - 1))
           atomicAdd(&hist[warp][sy], (uint32_t)__popc(peers));
@@ -111,13 +99,8 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
     }
   }
   if (part == parts - 1)
-    for (uint32_t i = nvec * kPer + tid; i < len; i += kHistThreads) {  // sample not a vector multiple
-      uint32_t sy;
-      if (DT == kF32) sy = (reinterpret_cast<const uint32_t *>(base)[i] >> 23) & 0xFFu;
-      else if (DT == kBF16) sy = (reinterpret_cast<const uint16_t *>(base)[i] >> 7) & 0xFFu;
-      else sy = reinterpret_cast<const uint16_t *>(base)[i] >> 8;
-      atomicAdd(&hist[warp][sy], 1u);
-    }
+    for (uint32_t i = nvec * kPer + tid; i < len; i += kHistThreads)  // sample not a vector multiple
+      atomicAdd(&hist[warp][symbol_at<DT>(base, i)], 1u);
   __syncthreads();
   uint32_t sum = 0;
 #pragma unroll
@@ -345,7 +328,7 @@ __device__ __forceinline__ uint4 narrow_vec(const float *acc) {
 // ================================================================ k_fused
 template <int DT, int B>
 struct FusedCfg {
-  static constexpr int kVec = (DT == kF32) ? 4 : 8;        // elements per 16-byte load
+  static constexpr int kVec = VecTraits<DT>::kSym;          // symbols per 16-byte load
   static constexpr int kIters = B / (32 * kVec);            // loads per lane per block
   static constexpr int kBatch = kIters < 8 ? kIters : 8;
   static constexpr int kRounds = B / 32;
@@ -405,7 +388,7 @@ static __device__ void finalize_stream(const EncJob &J, unsigned long long paylo
     if (J.wire_acc) atomicAdd(J.wire_acc, (unsigned long long)total * J.nd);
   }
   const uint64_t e1 = g.off_coff + 8 * g.n_chunks, e2 = g.off_dir + 4 * g.n_blocks;
-  const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+  const uint64_t tail_bytes = g.tail_bytes();
   const uint8_t *tsrc = J.in + g.n_coded * g.eb;
   for (uint32_t d = 0; d < J.nd; ++d) {
     uint8_t *o = J.dst[d];
@@ -457,11 +440,16 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
             }
           }
         }
+      } else if (DT == kE5M2) {  // R24: the bytes are the symbols, no residual plane
+        *reinterpret_cast<uint4 *>(sp) = v[i];
       } else {
         uint32_t s0, s1, q0, q1;
         if (DT == kBF16) {
           split4_bf16(v[i].x, v[i].y, s0, q0);
           split4_bf16(v[i].z, v[i].w, s1, q1);
+        } else if (DT == kE4M3) {
+          split4_e4m3(v[i].x, v[i].y, s0, q0);
+          split4_e4m3(v[i].z, v[i].w, s1, q1);
         } else {
           split4_f16(v[i].x, v[i].y, s0, q0);
           split4_f16(v[i].z, v[i].w, s1, q1);
@@ -660,7 +648,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   }
 
   const uint64_t b = b0 + warp;
-  const uint8_t *src = J.in + b * (uint64_t)B * elem_bytes(DT);
+  const uint8_t *src = J.in + b * (uint64_t)B * group_bytes(DT);
   uint32_t size = 0, kdir = 0, K = 0, x = kL;
   bool raw = false, ovf = false;
   if (b < g.n_blocks) {
@@ -920,7 +908,7 @@ static __device__ void forward_tile(const Plan &P, const DecJob &J, uint64_t t, 
     fwd_range(J, stream, 0, kHeaderBytes);
     fwd_range(J, stream, g.off_coff + 8 * g.n_chunks, g.off_dir - (g.off_coff + 8 * g.n_chunks));
     fwd_range(J, stream, g.off_dir + 4 * g.n_blocks, g.off_pay - (g.off_dir + 4 * g.n_blocks));
-    fwd_range(J, stream, g.off_tail(tile_end), (g.n - g.n_coded) * g.eb);
+    fwd_range(J, stream, g.off_tail(tile_end), g.tail_bytes());
   }
   __syncthreads();
   if (tid == 0) {
@@ -987,7 +975,7 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
   }
   if (bad && (threadIdx.x & 31) == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
   if (t == J.ntiles - 1) {  // raw tail
-    const uint64_t tail_bytes = (g.n - g.n_coded) * g.eb;
+    const uint64_t tail_bytes = g.tail_bytes();
     const uint8_t *tsrc = stream + g.off_tail(tile_end);
     uint8_t *tdst = J.out + g.n_coded * g.eb;
     for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
@@ -1201,8 +1189,12 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
       uint64_t k = it - ne - nc;  // job-major over the decode jobs
       int j = 0;
       while (j + 1 < P.nd_jobs && k >= P.d[j].ntiles) k -= P.d[j++].ntiles;
-      if (RED && P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
-      else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
+      if constexpr (RED) {
+        if (P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
+        else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
+      } else {
+        dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
+      }
     }
     __syncthreads();
     it = uniform_u64(S.tk[par ^ 1]);

@@ -24,13 +24,22 @@ constexpr int kWarps = 8;                       // warps per CTA in the codec ke
 constexpr uint32_t kTileBlocks = kWarps;        // blocks per look-back tile
 constexpr uint32_t kMaxB = 4096;                // largest block the GPU kernels stage in smem
 
-enum Dtype : int { kBF16 = 0, kF16 = 1, kF32 = 2 };
+enum Dtype : int { kBF16 = 0, kF16 = 1, kF32 = 2, kE4M3 = 3, kE5M2 = 4 };
+constexpr int kNumDtypes = 5;
 
-__host__ __device__ constexpr uint32_t elem_bytes(int dt) { return dt == kF32 ? 4u : 2u; }
+__host__ __device__ constexpr uint32_t elem_bytes(int dt) { return dt == kF32 ? 4u : (dt >= kE4M3 ? 1u : 2u); }
+// A symbol group is the input that yields one symbol: one element, or a pair
+// of e4m3 elements (R23).  Blocks, chunks and samples count groups.
+__host__ __device__ constexpr uint32_t group_elems(int dt) { return dt == kE4M3 ? 2u : 1u; }
+__host__ __device__ constexpr uint32_t group_bytes(int dt) { return elem_bytes(dt) * group_elems(dt); }
+// residual plane bytes per group (f32 has two planes: lo16 + hi8)
+__host__ __device__ constexpr uint32_t res_bytes(int dt) { return dt == kF32 ? 3u : (dt == kE5M2 ? 0u : 1u); }
 __host__ __device__ constexpr uint64_t round16(uint64_t v) { return (v + 15u) & ~uint64_t(15); }
 
 // Section offsets of a UZB1 stream, computed the same way
 // on host and device from the header fields.
+// n counts elements; n_blocks / n_coded count symbol groups; eb is the input
+// bytes per group (= element bytes except e4m3 pairs).
 struct StreamGeom {
   uint64_t n, n_blocks, n_coded, n_chunks;
   uint32_t B, CB, S, global, dtype, eb;
@@ -38,10 +47,10 @@ struct StreamGeom {
 
   __host__ __device__ void init(int dt, uint64_t n_, uint32_t B_, uint32_t CB_, uint32_t S_, bool global_) {
     dtype = (uint32_t)dt;
-    eb = elem_bytes(dt);
+    eb = group_bytes(dt);
     n = n_;
     B = B_;
-    n_blocks = n / B;
+    n_blocks = (n / group_elems(dt)) / B;
     n_coded = n_blocks * B;
     global = global_ ? 1u : 0u;
     if (global_) {
@@ -58,14 +67,16 @@ struct StreamGeom {
       off_tab = round16(off_res1 + n_coded);
     } else {
       off_res1 = off_res0;
-      off_tab = round16(off_res0 + n_coded);
+      off_tab = round16(off_res0 + res_bytes(dt) * n_coded);
     }
     off_coff = off_tab + 512 * n_chunks;
     off_dir = round16(off_coff + 8 * n_chunks);
     off_pay = round16(off_dir + 4 * n_blocks);
   }
   __host__ __device__ uint64_t off_tail(uint64_t payload) const { return round16(off_pay + payload); }
-  __host__ __device__ uint64_t total(uint64_t payload) const { return off_tail(payload) + (n - n_coded) * eb; }
+  // raw tail: the elements after the last whole block
+  __host__ __device__ uint64_t tail_bytes() const { return (n - n_coded * group_elems(dtype)) * elem_bytes(dtype); }
+  __host__ __device__ uint64_t total(uint64_t payload) const { return off_tail(payload) + tail_bytes(); }
   __host__ __device__ uint64_t n_tiles() const { return (n_blocks + kTileBlocks - 1) / kTileBlocks; }
   __host__ __device__ uint32_t chunk_blocks_of(uint64_t c) const {
     uint64_t left = n_blocks - c * CB;
@@ -206,6 +217,16 @@ __device__ __forceinline__ void st_any16(uint8_t *p, uint4 v) {
     for (int i = 0; i < 16; ++i) p[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
   }
 }
+__device__ __forceinline__ void st_any8(uint8_t *p, uint2 v) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 7) == 0) {
+    *reinterpret_cast<uint2 *>(p) = v;
+  } else {
+    const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+  }
+}
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
   return v;
@@ -270,6 +291,19 @@ __device__ __forceinline__ void join4_f16(uint32_t sym4, uint32_t res4, uint32_t
   w0 = __byte_perm(res4, sym4, 0x5140);
   w1 = __byte_perm(res4, sym4, 0x7362);
 }
+// e4m3 pairs (R23): 8 input bytes = 4 groups (a, b); symbol =
+// exp_a<<4 | exp_b, residual = s_a<<7 | m_a<<4 | s_b<<3 | m_b.
+__device__ __forceinline__ void split4_e4m3(uint32_t w0, uint32_t w1, uint32_t &sym4, uint32_t &res4) {
+  const uint32_t A = __byte_perm(w0, w1, 0x6420), Bv = __byte_perm(w0, w1, 0x7531);  // a's, b's
+  sym4 = ((A << 1) & 0xF0F0F0F0u) | ((Bv >> 3) & 0x0F0F0F0Fu);
+  res4 = (A & 0x80808080u) | ((A << 4) & 0x70707070u) | ((Bv >> 4) & 0x08080808u) | (Bv & 0x07070707u);
+}
+__device__ __forceinline__ void join4_e4m3(uint32_t sym4, uint32_t res4, uint32_t &w0, uint32_t &w1) {
+  const uint32_t A = (res4 & 0x80808080u) | ((sym4 >> 1) & 0x78787878u) | ((res4 >> 4) & 0x07070707u);
+  const uint32_t Bv = ((res4 << 4) & 0x80808080u) | ((sym4 << 3) & 0x78787878u) | (res4 & 0x07070707u);
+  w0 = __byte_perm(A, Bv, 0x5140);
+  w1 = __byte_perm(A, Bv, 0x7362);
+}
 __device__ __forceinline__ uint4 join4_f32(uint32_t sym4, uint2 lo, uint32_t hi4) {
   uint32_t b2 = ((sym4 << 7) & 0x80808080u) | (hi4 & 0x7F7F7F7Fu);
   uint32_t b3 = (hi4 & 0x80808080u) | ((sym4 >> 1) & 0x7F7F7F7Fu);
@@ -281,6 +315,42 @@ __device__ __forceinline__ uint4 join4_f32(uint32_t sym4, uint2 lo, uint32_t hi4
   r.z = __byte_perm(lo.y, h23, 0x5410);
   r.w = __byte_perm(lo.y, h23, 0x7632);
   return r;
+}
+
+// Symbols per 16-byte input vector, and the symbols of one vector as
+// little-endian symbol words (a1 for every dtype; residual planes are split
+// by the encoder itself).
+template <int DT>
+struct VecTraits {
+  static constexpr int kSym = DT == kF32 ? 4 : (DT == kE5M2 ? 16 : 8);
+};
+template <int DT>
+__device__ __forceinline__ void vec_symbols(uint4 w, uint32_t sw[4]) {
+  uint32_t r;
+  if (DT == kBF16) {
+    split4_bf16(w.x, w.y, sw[0], r);
+    split4_bf16(w.z, w.w, sw[1], r);
+  } else if (DT == kF16) {
+    split4_f16(w.x, w.y, sw[0], r);
+    split4_f16(w.z, w.w, sw[1], r);
+  } else if (DT == kE4M3) {
+    split4_e4m3(w.x, w.y, sw[0], r);
+    split4_e4m3(w.z, w.w, sw[1], r);
+  } else if (DT == kE5M2) {  // R24: every byte is a symbol
+    sw[0] = w.x, sw[1] = w.y, sw[2] = w.z, sw[3] = w.w;
+  } else {
+    uint2 lo;
+    split4_f32(w, sw[0], lo, r);
+  }
+}
+// symbol i of a group-ordered input (scalar tail of a sample)
+template <int DT>
+__device__ __forceinline__ uint32_t symbol_at(const uint8_t *base, uint32_t i) {
+  if (DT == kF32) return (reinterpret_cast<const uint32_t *>(base)[i] >> 23) & 0xFFu;
+  if (DT == kBF16) return (reinterpret_cast<const uint16_t *>(base)[i] >> 7) & 0xFFu;
+  if (DT == kF16) return reinterpret_cast<const uint16_t *>(base)[i] >> 8;
+  if (DT == kE5M2) return base[i];
+  return (((uint32_t)base[2 * i] << 1) & 0xF0u) | (((uint32_t)base[2 * i + 1] >> 3) & 0x0Fu);  // e4m3 pair
 }
 
 // ---------------------------------------------------------------- a3 encode table entry

@@ -16,9 +16,12 @@ import torch
 import synth
 
 pytestmark = pytest.mark.gpu
-BF16, F16, F32 = 0, 1, 2
-TD = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32}
-VIEW = {BF16: torch.int16, F16: torch.int16, F32: torch.int32}
+BF16, F16, F32, E4M3, E5M2 = 0, 1, 2, 3, 4
+TD = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32, E4M3: torch.float8_e4m3fn,
+      E5M2: torch.float8_e5m2}
+VIEW = {BF16: torch.int16, F16: torch.int16, F32: torch.int32, E4M3: torch.uint8, E5M2: torch.uint8}
+NPV = {BF16: np.int16, F16: np.int16, F32: np.int32, E4M3: np.uint8, E5M2: np.uint8}
+NPU = {BF16: np.uint16, F16: np.uint16, F32: np.uint32, E4M3: np.uint8, E5M2: np.uint8}
 
 
 @pytest.fixture(scope="module")
@@ -31,12 +34,12 @@ def uz():
 
 
 def to_dev(bits: np.ndarray, dtype: int) -> torch.Tensor:
-    t = torch.from_numpy(bits.view(np.int32 if dtype == F32 else np.int16).copy())
+    t = torch.from_numpy(np.ascontiguousarray(bits).view(NPV[dtype]).copy())
     return t.view(TD[dtype]).cuda()
 
 
 def to_bits(t: torch.Tensor, dtype: int) -> np.ndarray:
-    return t.view(VIEW[dtype]).cpu().numpy().view(np.uint32 if dtype == F32 else np.uint16)
+    return t.view(VIEW[dtype]).cpu().numpy().view(NPU[dtype])
 
 
 def gpu_compress(uz, bits, dtype, **params) -> bytes:
@@ -234,3 +237,42 @@ def test_encoder_word_overflow_rare_path(uz, orc, dtype):
     assert got == ref
     st, back = gpu_decompress(uz, got, bits.size, dtype)
     assert st == 0 and np.array_equal(back, bits)
+
+
+
+FP8_GENS = {
+    "U": lambda n, s, d: synth.uniform(n, s, d),
+    "W": lambda n, s, d: synth.normal(n, 0.02, s, d),
+    "special": lambda n, s, d: synth.special_mix(n, s, d),
+    "random": lambda n, s, d: synth.random_bits(n, s, d),
+}
+
+
+@pytest.mark.parametrize("dtype", [E4M3, E5M2])
+@pytest.mark.parametrize("n", [0, 1, 2, 4095, 8191, 8192, 8193, 3 * 8192 + 7, 80 * 4096 + 3])
+@pytest.mark.parametrize("dist", list(FP8_GENS))
+def test_fp8_stream_bytes_equal_oracle(uz, orc, dtype, n, dist):
+    """fp8 codecs (R23 e4m3 pairs, R24 e5m2 bytes): GPU stream == oracle stream."""
+    bits = FP8_GENS[dist](n, 3000 + n, dtype)
+    ref = orc.compress(dtype, bits)
+    got = gpu_compress(uz, bits, dtype)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, n, dtype)
+    assert st == 0 and np.array_equal(back, bits)
+
+
+@pytest.mark.parametrize("dtype", [E4M3, E5M2])
+@pytest.mark.parametrize("params", [dict(block_symbols=1024), dict(global_table=True),
+                                    dict(chunk_blocks=8, sample_symbols=5000, block_symbols=2048)])
+def test_fp8_stream_params_equal_oracle(uz, orc, dtype, params):
+    n = 45 * 4096 + 11
+    bits = synth.normal(n, 0.02, 9, dtype)
+    bits[4096 * 10:4096 * 12] = synth.random_bits(8192, 10, dtype)
+    assert gpu_compress(uz, bits, dtype, **params) == orc.compress(dtype, bits, **params)
+
+
+def test_fp8_multichunk_48mib(uz, orc):
+    for dtype in (E4M3, E5M2):
+        n = (48 << 20) + 123
+        bits = synth.normal(n, 0.02, 4, dtype)
+        assert gpu_compress(uz, bits, dtype) == orc.compress(dtype, bits)

@@ -20,10 +20,12 @@ import torch
 import synth
 
 pytestmark = pytest.mark.gpu
-BF16, F16, F32 = 0, 1, 2
-TD = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32}
-VIEW = {BF16: torch.int16, F16: torch.int16, F32: torch.int32}
-NPU = {BF16: np.uint16, F16: np.uint16, F32: np.uint32}
+BF16, F16, F32, E4M3, E5M2 = 0, 1, 2, 3, 4
+TD = {BF16: torch.bfloat16, F16: torch.float16, F32: torch.float32, E4M3: torch.float8_e4m3fn,
+      E5M2: torch.float8_e5m2}
+VIEW = {BF16: torch.int16, F16: torch.int16, F32: torch.int32, E4M3: torch.uint8, E5M2: torch.uint8}
+NPU = {BF16: np.uint16, F16: np.uint16, F32: np.uint32, E4M3: np.uint8, E5M2: np.uint8}
+NPV = {BF16: np.int16, F16: np.int16, F32: np.int32, E4M3: np.uint8, E5M2: np.uint8}
 
 
 @pytest.fixture(scope="module")
@@ -36,7 +38,7 @@ def uz():
 
 
 def dev(bits, dtype):
-    t = torch.from_numpy(np.ascontiguousarray(bits).view(np.int32 if dtype == F32 else np.int16).copy())
+    t = torch.from_numpy(np.ascontiguousarray(bits).view(NPV[dtype]).copy())
     return t.view(TD[dtype]).cuda()
 
 
@@ -292,7 +294,7 @@ def test_broadcast_relay_wire_streams_equal_oracle(uz, orc):
         bufs = [dev(bits, BF16) if r == root else torch.empty(n, dtype=torch.bfloat16, device="cuda")
                 for r in range(nr)]
         g.run(lambda r, c, s: c.broadcast(bufs[r], root, s))
-        P = ((n + 1) // 2 + 7) // 8 * 8
+        P = ((n + 1) // 2 + 15) // 16 * 16  # pieces of 16 elements (comm.cu)
         pieces = [bits[:P], bits[P:]]
         refs = [orc.compress(BF16, pc) for pc in pieces]
         # piece 0 -> rank 1 from root; rank 1 relays it to rank 2 (src 1); piece 1 -> rank 2, relayed to rank 1
@@ -369,5 +371,46 @@ def test_p2p_large_full_occupancy(uz, max_ctas):
                 print("ERROR_DETAIL", [c.error_detail() for c in g.comms], flush=True)
             assert errs == [0, 0]
             assert torch.equal(x.view(torch.int16), y.view(torch.int16))
+    finally:
+        g.close()
+
+
+
+@pytest.mark.parametrize("dtype", [E4M3, E5M2])
+def test_fp8_p2p_allgather_alltoall_broadcast(uz, orc, dtype):
+    """fp8 on the communication path (R22): P2P (with the wire stream == oracle), allgather with
+    ragged counts, all-to-all and the relayed broadcast are bit-exact; reductions are rejected."""
+    nr = 3
+    g = Group(uz, nr, staging_bytes=32 << 20, min_compress_bytes=1)
+    try:
+        n = 3 * (1 << 20) + 4096 * 2 + 5
+        bits = gen("W", n, 70, dtype)
+        x = dev(bits, dtype)
+        y = torch.empty_like(x)
+        g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else (c.recv(y, 0, s) if r == 1 else None))
+        assert np.array_equal(host(y, dtype), bits)
+        ref = orc.compress(dtype, bits)
+        assert g.comms[1].read_staging(0, 0, len(ref)) == ref
+        m = (1 << 20) + 4096 + 3
+        ins = [gen("U", m, 80 + r, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(nr * m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_gather(outs[r], xs[r], s))
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], dtype), np.concatenate(ins))
+        cc = (1 << 20) + 32
+        a2a_in = [gen("W", nr * cc, 90 + r, dtype) for r in range(nr)]
+        a2a_x = [dev(b, dtype) for b in a2a_in]
+        a2a_o = [torch.empty(nr * cc, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_to_all(a2a_o[r], a2a_x[r], s))
+        for r in range(nr):
+            assert np.array_equal(host(a2a_o[r], dtype),
+                                  np.concatenate([a2a_in[i][r * cc:(r + 1) * cc] for i in range(nr)]))
+        bufs = [dev(bits, dtype) if r == 0 else torch.empty(n, dtype=TD[dtype], device="cuda") for r in range(nr)]
+        g.run(lambda r, c, s: c.broadcast(bufs[r], 0, s))
+        for r in range(nr):
+            assert np.array_equal(host(bufs[r], dtype), bits)
+        with pytest.raises(uz.UzipError):
+            g.comms[0].all_reduce(xs[0][: 3 * 4096])
     finally:
         g.close()
