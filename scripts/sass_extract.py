@@ -41,7 +41,9 @@ def main():
         if not ins:
             continue
         ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", t).split()[0] for _, t in ins)
-        votes = [i for i, (_, t) in enumerate(ins) if "VOTE.ANY R" in t]
+        # the fast-path rounds: VOTEs outside the compiler's divergent fallback (WARPSYNC.COLLECTIVE) blocks
+        votes = [i for i, (_, t) in enumerate(ins) if "VOTE.ANY R" in t
+                 and "WARPSYNC.COLLECTIVE" not in ins[i - 1][1]]
         best, lo = 0, 0
         for i in range(len(votes)):  # densest window of 12 consecutive VOTEs
             j = min(len(votes) - 1, i + 11)
