@@ -414,3 +414,32 @@ def test_fp8_p2p_allgather_alltoall_broadcast(uz, orc, dtype):
             g.comms[0].all_reduce(xs[0][: 3 * 4096])
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("codec", [dict(block_symbols=1024), dict(block_symbols=2048, chunk_blocks=16),
+                                   dict(global_table=True)])
+def test_collectives_with_codec_params(uz, orc, codec):
+    """The wire format's parameters (block size, chunk size, global table) flow through the
+    communicator: P2P wire stream == oracle stream with the same params; allreduce bit-exact."""
+    nr = 2
+    g = Group(uz, nr, staging_bytes=64 << 20, min_compress_bytes=1, **codec)
+    try:
+        n = 3 * (1 << 20) + 4096 * 7 + 11
+        bits = synth.weights(n, 123)
+        x = dev(bits, BF16)
+        y = torch.empty_like(x)
+        g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else c.recv(y, 0, s))
+        assert np.array_equal(host(y, BF16), bits)
+        ref = orc.compress(BF16, bits, **codec)
+        assert g.comms[1].read_staging(0, 0, len(ref)) == ref
+        m = nr * ((1 << 20) + 4096 * 3 + 8)
+        ins = [synth.activations(m // 4096, 300 + r)[:m] if m % 4096 == 0 else synth.weights(m, 300 + r)
+               for r in range(nr)]
+        xs = [dev(b, BF16) for b in ins]
+        outs = [torch.empty(m, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_reduce(outs[r], xs[r], s))
+        refar = orc.allreduce(BF16, ins)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], BF16), refar)
+    finally:
+        g.close()
