@@ -175,6 +175,8 @@ void base_plan(uzip_comm *c, Plan &p, int dt) {
   p.ticket = ws_ticket(c);
   p.err = reinterpret_cast<uint32_t *>(c->region);
   p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
+  static const uint32_t stress = (uint32_t)strtoul(getenv("UZIP_STRESS") ? getenv("UZIP_STRESS") : "0", nullptr, 0);
+  p.stress = stress;
 }
 
 // Encode job of `n` elements at `in` (round stream) into destinations dsts.

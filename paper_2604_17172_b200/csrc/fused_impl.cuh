@@ -188,6 +188,15 @@ __device__ __forceinline__ void raise_err_at(const Plan &P, uint32_t code, uint3
   }
 }
 
+// Debug stress (UZIP_STRESS=seed): a pseudo-random pause of up to ~16 us at the protocol's hand-off
+// points, so the loopback tests exercise late flags, early credits and reordered tiles.
+__device__ __forceinline__ void stress_pause(const Plan &P, uint64_t salt) {
+  if (!P.stress) return;
+  uint64_t h = (salt + P.stress) * 0x9E3779B97F4A7C15ull + blockIdx.x * 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 31;
+  if ((h & 3) == 0) __nanosleep((unsigned)((h >> 8) & 0x3FFF));
+}
+
 // Poll a tile flag until its epoch matches (thread-level; bounded by the
 // plan's timeout, aborts when another CTA raised an error).
 static __device__ bool wait_flag(const Plan &P, const unsigned long long *f, uint32_t epoch, unsigned long long &v) {
@@ -582,7 +591,10 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
           S.tile_cnt = 0;
           const unsigned long long off16 = tile_off >> 4;
           for (uint32_t d = 0; d < J.nd; ++d)
-            if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+            if (J.flag[d]) {
+            stress_pause(P, t * 7 + d);
+            st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+          }
         }
       }
     }
@@ -629,7 +641,10 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
     if (tid == 0 && flags) {
       __threadfence_system();
       for (uint32_t d = 0; d < J.nd; ++d)
-        if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
+        if (J.flag[d]) {
+          stress_pause(P, t * 11 + d);
+          st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
+        }
     }
     return;
   }
@@ -766,7 +781,10 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
         S.tile_cnt = 0;
         const unsigned long long off16 = tile_off >> 4;
         for (uint32_t d = 0; d < J.nd; ++d)
-          if (J.flag[d]) st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+          if (J.flag[d]) {
+            stress_pause(P, t * 7 + d);
+            st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
+          }
       }
     }
   }
@@ -799,6 +817,7 @@ static __device__ void dec_done(const DecJob &J) {
 // carries the table, when the table is not cached).  Sets S.abort on failure.
 static __device__ void acquire_tile(const Plan &P, const DecJob &J, uint32_t s, uint64_t t, bool need_table,
                              FusedShared &S) {
+  stress_pause(P, t * 131 + s);
   unsigned long long v = 0;
   bool ok = wait_flag(P, J.flag[s] + t, J.epoch[s], v);
   S.src_off[s] = (v & 0xFFFFFFFFull) << 4;

@@ -89,6 +89,7 @@ struct Plan {
   uint32_t *err;                            // sticky async error word
   uint64_t timeout_ns;
   int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
+  uint32_t stress;                          // debug: != 0 injects pseudo-random delays (UZIP_STRESS)
 };
 
 // k_hist splits a chunk's sample over up to kMaxHistParts CTAs of >= 16 Ki symbols.

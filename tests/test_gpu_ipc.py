@@ -35,3 +35,16 @@ def test_bench_dist_smoke_two_processes_same_gpu():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["compression_ratio"] < 0.75
+
+
+def test_protocol_under_random_delays():
+    """Race shake-out: the loopback collectives re-run with UZIP_STRESS, which injects
+    pseudo-random pauses of up to ~16 us before tile-flag releases and tile acquires."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, UZIP_STRESS="4242")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_comm.py"), "-k",
+           "p2p_many_rounds or allgather or allreduce or broadcast or alltoall or reduce_scatter"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
