@@ -82,6 +82,7 @@ def lib():
         l.uzo_decompress.argtypes = [vp, sz, vp, sz, i32]
         l.uzo_decompress.restype = i32
         l.uzo_reduce_sum.argtypes = [i32, ctypes.POINTER(vp), i32, sz, vp]
+        l.uzo_reduce.argtypes = [i32, i32, ctypes.POINTER(vp), i32, sz, vp]
         l.uzo_round_from_f32.argtypes = [i32, ctypes.c_float]
         l.uzo_round_from_f32.restype = u32
         l.uzo_widen_to_f32.argtypes = [i32, u32]
@@ -225,6 +226,19 @@ def sections(stream: bytes) -> dict:
 
 
 # ---------------------------------------------------------------- a9 fold
+SUM, MIN, MAX = 0, 1, 2
+
+
+def reduce(dtype: int, inputs, op: int = 0) -> np.ndarray:
+    """Fold R with op (R11 sum; R25 min/max), rank order."""
+    arrs = [np.ascontiguousarray(a, dtype=NP_UINT[dtype]).reshape(-1) for a in inputs]
+    n = arrs[0].size
+    ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    out = np.zeros(max(n, 1), NP_UINT[dtype])
+    lib().uzo_reduce(dtype, op, ptrs, len(arrs), n, _ptr(out))
+    return out[:n]
+
+
 def reduce_sum(dtype: int, inputs) -> np.ndarray:
     arrs = [np.ascontiguousarray(a, dtype=NP_UINT[dtype]).reshape(-1) for a in inputs]
     n = arrs[0].size
@@ -247,11 +261,11 @@ def allgather(dtype: int, inputs):
     return np.concatenate([np.asarray(a, NP_UINT[dtype]).reshape(-1) for a in inputs])
 
 
-def reduce_scatter(dtype: int, inputs, nranks: int):
+def reduce_scatter(dtype: int, inputs, nranks: int, op: int = 0):
     """ReduceScatter: rank r gets R over shard r of every input."""
     n = np.asarray(inputs[0]).size // nranks
-    return [reduce_sum(dtype, [np.asarray(a).reshape(-1)[r * n:(r + 1) * n] for a in inputs]) for r in range(nranks)]
+    return [reduce(dtype, [np.asarray(a).reshape(-1)[r * n:(r + 1) * n] for a in inputs], op) for r in range(nranks)]
 
 
-def allreduce(dtype: int, inputs):
-    return reduce_sum(dtype, inputs)
+def allreduce(dtype: int, inputs, op: int = 0):
+    return reduce(dtype, inputs, op)

@@ -586,6 +586,39 @@ uint32_t uzo_round_from_f32(int dtype, float v) {
   return w;
 }
 
+/* min / max fold ("sum, min, or max"; reading R25): IEEE 754-2019
+ * minimum/maximum in rank order -- a NaN operand makes the result NaN
+ * (canonical on output), -0 < +0, otherwise the smaller / larger value.
+ * The result is one of the inputs, so the final rounding is exact. */
+static float fold_min(float acc, float x) {
+  if (isnan(acc) || isnan(x)) return NAN;
+  if (x < acc) return x;
+  if (x == acc && signbit(x) && !signbit(acc)) return x; /* -0 beats +0 */
+  return acc;
+}
+static float fold_max(float acc, float x) {
+  if (isnan(acc) || isnan(x)) return NAN;
+  if (x > acc) return x;
+  if (x == acc && !signbit(x) && signbit(acc)) return x; /* +0 beats -0 */
+  return acc;
+}
+
+void uzo_reduce(int dtype, int op, const void *const *inputs, int nranks, size_t n, void *out_v) {
+  if (op == UZO_OP_SUM) {
+    uzo_reduce_sum(dtype, inputs, nranks, n, out_v);
+    return;
+  }
+  uint8_t *out = (uint8_t *)out_v;
+  for (size_t i = 0; i < n; ++i) {
+    float acc = uzo_widen_to_f32(dtype, load_elem(dtype, (const uint8_t *)inputs[0], i));
+    for (int k = 1; k < nranks; ++k) {
+      float xk = uzo_widen_to_f32(dtype, load_elem(dtype, (const uint8_t *)inputs[k], i));
+      acc = op == UZO_OP_MIN ? fold_min(acc, xk) : fold_max(acc, xk);
+    }
+    store_elem(dtype, out, i, uzo_round_from_f32(dtype, acc));
+  }
+}
+
 void uzo_reduce_sum(int dtype, const void *const *inputs, int nranks, size_t n, void *out_v) {
   uint8_t *out = (uint8_t *)out_v;
   for (size_t i = 0; i < n; ++i) {

@@ -106,6 +106,11 @@ int uzo_decompress(const uint8_t *in, size_t in_bytes, void *out, size_t n, int 
  * n elements. */
 void uzo_reduce_sum(int dtype, const void *const *inputs, int nranks, size_t n, void *out);
 
+/* a9 with op (R25): UZO_OP_SUM is the fold above; UZO_OP_MIN / UZO_OP_MAX are IEEE 754-2019
+ * minimum / maximum in rank order (NaN propagates, -0 < +0); same output rounding. */
+enum { UZO_OP_SUM = 0, UZO_OP_MIN = 1, UZO_OP_MAX = 2 };
+void uzo_reduce(int dtype, int op, const void *const *inputs, int nranks, size_t n, void *out);
+
 /* fp32 -> dtype rounding used by the fold (exported for its pin test). */
 uint32_t uzo_round_from_f32(int dtype, float v);
 float uzo_widen_to_f32(int dtype, uint32_t bits);
