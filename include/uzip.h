@@ -44,8 +44,9 @@ extern "C" {
  * bytes are symbols (R24); fp8 is not reduced (reduce-scatter / allreduce, R22). */
 typedef enum { UZIP_BF16 = 0, UZIP_F16 = 1, UZIP_F32 = 2, UZIP_E4M3 = 3, UZIP_E5M2 = 4 } uzip_dtype_t;
 
-/* Reduction operators (P:402 names sum, min, max; this build: sum, R11). */
-typedef enum { UZIP_SUM = 0 } uzip_op_t;
+/* Reduction operators ("sum, min, or max"): the fold R in rank order -- sum in fp32 with
+ * one rounding (R11); min / max = IEEE 754-2019 minimum / maximum, NaN propagates, -0 < +0 (R25). */
+typedef enum { UZIP_SUM = 0, UZIP_MIN = 1, UZIP_MAX = 2 } uzip_op_t;
 
 typedef enum {
   UZIP_OK = 0,

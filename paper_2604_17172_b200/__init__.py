@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("UZIP_LIB_PATH") or os.path.join(_HERE, "libuzip.so")  # override: tuning variants
 
 BF16, F16, F32, E4M3, E5M2 = 0, 1, 2, 3, 4
-SUM = 0
+SUM, MIN, MAX = 0, 1, 2
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED_DTYPE", 3: "CAPACITY", 4: "CORRUPT_STREAM",
           5: "SIZE_MISMATCH", 6: "CUDA", 7: "COMM", 8: "TIMEOUT", 9: "NOT_IMPLEMENTED"}
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED_DTYPE, ERR_CAPACITY, ERR_CORRUPT_STREAM, ERR_SIZE_MISMATCH, \
@@ -325,15 +325,15 @@ class Comm:
         _check(lib().uzip_allgather(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), inp.numel(),
                                     uz_dtype(inp.dtype), self.h, _stream(stream)), "uzip_allgather")
 
-    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, stream=None):
+    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, stream=None, op: int = SUM):
         _check(lib().uzip_reduce_scatter(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                         out.numel(), uz_dtype(inp.dtype), SUM, self.h, _stream(stream)),
+                                         out.numel(), uz_dtype(inp.dtype), op, self.h, _stream(stream)),
                "uzip_reduce_scatter")
 
-    def all_reduce(self, out: torch.Tensor, inp: torch.Tensor | None = None, stream=None):
+    def all_reduce(self, out: torch.Tensor, inp: torch.Tensor | None = None, stream=None, op: int = SUM):
         inp = out if inp is None else inp
         _check(lib().uzip_allreduce(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), out.numel(),
-                                    uz_dtype(out.dtype), SUM, self.h, _stream(stream)), "uzip_allreduce")
+                                    uz_dtype(out.dtype), op, self.h, _stream(stream)), "uzip_allreduce")
 
     def all_to_all(self, out: torch.Tensor, inp: torch.Tensor, stream=None):
         """out[i*c:(i+1)*c] <- rank i's inp[me*c:(me+1)*c], c = inp.numel() // nranks."""

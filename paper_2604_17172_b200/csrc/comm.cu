@@ -486,7 +486,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
                                   uzip_op_t op, uzip_comm_t c, void *stream) {
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
-  if (op != UZIP_SUM) return UZIP_ERR_INVALID_ARG;
+  if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
   if (recvcount == 0) return UZIP_OK;
   if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
   const int dt = (int)dtype;
@@ -520,6 +520,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
       p.c.ntiles = (p.c.bytes + kRawTileBytes - 1) / kRawTileBytes;
     } else {
       dec_job(c, p, 0, dt, n, comp, all, me, in + ((uint64_t)me * recvcount + o) * eb, out + o * eb);
+      p.d[0].op = (uint32_t)op;
     }
     if (uzip_status_t s = launch(c, p, comp, st)) return s;
   }
@@ -530,7 +531,7 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
                              uzip_comm_t c, void *stream) {
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
-  if (op != UZIP_SUM) return UZIP_ERR_INVALID_ARG;
+  if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
   if (count == 0) return UZIP_OK;
   const int N = c->nranks;
   if (count % (size_t)N != 0) return UZIP_ERR_INVALID_ARG;

@@ -303,20 +303,29 @@ __device__ __forceinline__ uint32_t narrow(float v) {
   if (DT == kF16) return (uint32_t)__half_as_ushort(__float2half_rn(v));
   return __float_as_uint(v);
 }
-__device__ __forceinline__ float fold(float acc, float x, bool first) { return first ? x : __fadd_rn(acc, x); }
+// One fold step of R (rank order): op 0 = fp32 sum without FMA contraction (R11); 1 / 2 = IEEE
+// 754-2019 minimum / maximum (R25: NaN propagates, -0 < +0; canonicalised by narrow()).
+__device__ __forceinline__ float fold(float acc, float x, bool first, uint32_t op) {
+  if (first) return x;
+  if (op == 0) return __fadd_rn(acc, x);
+  if (acc != acc || x != x) return __int_as_float(0x7FFFFFFF);
+  const bool sx = signbit(x), sa = signbit(acc);
+  if (op == 1) return (x < acc || (x == acc && sx && !sa)) ? x : acc;
+  return (x > acc || (x == acc && !sx && sa)) ? x : acc;
+}
 
 // Fold 16 bytes of elements into acc[0..kPer) (kPer = 8 for 2-byte types, 4 for fp32).
 template <int DT>
-__device__ __forceinline__ void fold_vec(float *acc, uint4 v, bool first) {
+__device__ __forceinline__ void fold_vec(float *acc, uint4 v, bool first, uint32_t op) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   if (DT == kF32) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] = fold(acc[i], widen<DT>(w[i]), first);
+    for (int i = 0; i < 4; ++i) acc[i] = fold(acc[i], widen<DT>(w[i]), first, op);
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      acc[2 * i] = fold(acc[2 * i], widen<DT>(w[i] & 0xFFFFu), first);
-      acc[2 * i + 1] = fold(acc[2 * i + 1], widen<DT>(w[i] >> 16), first);
+      acc[2 * i] = fold(acc[2 * i], widen<DT>(w[i] & 0xFFFFu), first, op);
+      acc[2 * i + 1] = fold(acc[2 * i + 1], widen<DT>(w[i] >> 16), first, op);
     }
   }
 }
@@ -1009,6 +1018,7 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
 struct FoldEpi {
   float *acc;
   bool first;
+  uint32_t op;
   template <int DT>
   __device__ __forceinline__ void apply(uint32_t e0, uint4 a, uint4 b) const {
     float v[8];
@@ -1016,10 +1026,10 @@ struct FoldEpi {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = acc[e0 + i];
     if (DT == kF32) {
-      fold_vec<DT>(v, a, first);
-      fold_vec<DT>(v + 4, b, first);
+      fold_vec<DT>(v, a, first, op);
+      fold_vec<DT>(v + 4, b, first, op);
     } else {
-      fold_vec<DT>(v, a, first);
+      fold_vec<DT>(v, a, first, op);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[e0 + i] = v[i];
@@ -1051,7 +1061,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
       for (uint32_t s = 0; s < J.nsrc; ++s) {
         const uint8_t *p = J.src[s] + o0 + 16 * i;
         const uint4 v = ((int32_t)s == J.me) ? ldg_nc_v4(p) : ld_cg_v4(p);
-        fold_vec<DT>(acc, v, s == 0);
+        fold_vec<DT>(acc, v, s == 0, J.op);
       }
       *reinterpret_cast<uint4 *>(J.out + o0 + 16 * i) = narrow_vec<DT>(acc);
     }
@@ -1061,7 +1071,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
         const uint8_t *p = J.src[s] + o0 + i * eb;
         const uint32_t bits = DT == kF32 ? *reinterpret_cast<const uint32_t *>(p)
                                          : (uint32_t)*reinterpret_cast<const uint16_t *>(p);
-        acc = fold(acc, widen<DT>(bits), s == 0);
+        acc = fold(acc, widen<DT>(bits), s == 0, J.op);
       }
       const uint32_t r = narrow<DT>(acc);
       if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + o0 + i * eb) = r;
@@ -1090,7 +1100,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
           float a[8];
           if (!first)
             for (int i = 0; i < kPer; ++i) a[i] = acc[e + i];
-          fold_vec<DT>(a, ldg_nc_v4(src + e * eb), first);
+          fold_vec<DT>(a, ldg_nc_v4(src + e * eb), first, J.op);
           for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
         }
       }
@@ -1121,7 +1131,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     if (b < g.n_blocks && !tb) {
       const uint32_t size = K == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * K);
       stage_payload(stream, g, off, size, pay);
-      FoldEpi epi{acc, first};
+      FoldEpi epi{acc, first, J.op};
       if (K != kRawBlock) {
         if (!decode_join_warp_epi<DT, B>(pay, K, dtab, symb, stream, g, b, epi)) bad = true;
       } else {  // stored-raw block: symbols are the payload
@@ -1165,7 +1175,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
                                                 : J.src[s] + g.off_tail(S.src_payload[s]) + i * eb;
         const uint32_t bits = DT == kF32 ? *reinterpret_cast<const uint32_t *>(p)
                                          : (uint32_t)*reinterpret_cast<const uint16_t *>(p);
-        a = fold(a, widen<DT>(bits), s == 0);
+        a = fold(a, widen<DT>(bits), s == 0, J.op);
       }
       const uint32_t r = narrow<DT>(a);
       if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + (g.n_coded + i) * eb) = r;

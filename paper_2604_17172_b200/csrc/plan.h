@@ -56,7 +56,7 @@ struct DecJob {
   uint32_t raw;
   uint32_t nsrc;                            // 1: plain decode; > 1: decode + reduce over sources
   int32_t me;                               // reduce: index of the local (uncompressed) source, -1 none
-  uint32_t pad_;
+  uint32_t op;                              // reduce: 0 sum, 1 min, 2 max (R11, R25)
   const uint8_t *src[kMaxRanks];            // stream base in local staging (me: local raw input)
   const unsigned long long *flag[kMaxRanks];  // local tile flags per source
   unsigned long long *credit[kMaxRanks];    // word at the source to release when the round is consumed

@@ -212,6 +212,46 @@ def test_allreduce_in_place_and_transparency(uz, orc):
         assert np.array_equal(results["off"][r], ref)
 
 
+@pytest.mark.parametrize("op", [1, 2])  # UZIP_MIN, UZIP_MAX (R25)
+@pytest.mark.parametrize("nr", [2, 3])
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("compress", [True, False])
+def test_min_max_reduce_scatter_and_allreduce(uz, orc, op, nr, dtype, compress):
+    """min / max folds (NaN propagates, -0 < +0) on the compressed and the raw path == oracle."""
+    cfg = dict(CFG_SMALL) if compress else dict(staging_bytes=8 << 20, min_compress_bytes=(1 << 64) - 1)
+    g = Group(uz, nr, **cfg)
+    try:
+        m = (1 << 19) + 4096 + 8
+        ins = [gen("special" if r % 2 else "W", nr * m, 3100 + 7 * r + op, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.reduce_scatter(outs[r], xs[r], s, op=op))
+        ref = orc.reduce_scatter(dtype, ins, nr, op)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], dtype), ref[r]), r
+        assert g.comms[0].stats()["compressed"] == compress
+        ar = [torch.empty(nr * m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_reduce(ar[r], xs[r], s, op=op))
+        ref = orc.allreduce(dtype, ins, op)
+        for r in range(nr):
+            assert np.array_equal(host(ar[r], dtype), ref), r
+    finally:
+        g.close()
+
+
+def test_reduce_rejects_unknown_op_and_fp8(uz):
+    g = Group(uz, 2, **CFG_SMALL)
+    try:
+        x = torch.zeros(2 * 4096, dtype=torch.bfloat16, device="cuda")
+        with pytest.raises(uz.UzipError):
+            g.comms[0].all_reduce(x, None, None, op=3)
+        f = torch.zeros(2 * 4096, dtype=torch.float8_e4m3fn, device="cuda")
+        with pytest.raises(uz.UzipError):
+            g.comms[0].all_reduce(f, None, None, op=1)
+    finally:
+        g.close()
+
+
 def test_reduce_scatter_rejects_unaligned_shards(uz):
     g = Group(uz, 2, **CFG_SMALL)
     try:
