@@ -135,6 +135,25 @@ def run(args):
         ablation = {"encode_send_GBps": round(raw / (ms_es / 1e3) / GB, 3), "ms": round(ms_es, 4),
                     "note": "uzip_compress + NCCL send of the stream + uzip_decompress, serial"}
 
+        # chunked pipeline (one stream and one launch per 8 MiB chunk) and SM-limited runs
+        # (fig:resource_usage; a CTA cap per side stands in for Green Contexts): same calls, other configs
+        def p2p_with(**cfg):
+            cm = uz.Comm.from_group(None, local, **cfg)
+
+            def step():
+                with torch.cuda.stream(stream):
+                    if role == "send":
+                        cm.send(x, peer, stream)
+                    elif role == "recv":
+                        cm.recv(y, peer, stream)
+            t = _timed(step, stream, args.steps, args.warmup)
+            assert cm.async_error() == 0
+            cm.destroy()
+            return round(raw / (t / 1e3) / GB, 3)
+
+        ablation["chunked_8MiB_GBps"] = p2p_with(pipe_chunk_bytes=8 << 20)
+        ablation["sm_limited_GBps"] = {str(m): p2p_with(max_ctas=m) for m in (16, 37, 74, 148)}
+
     # e2e through the public API with host buffers: the sender copies its input from pinned host memory
     # and sends; the receiver receives and reads 16 bytes of the result back; wall clock, max over ranks
     host = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)

@@ -20,8 +20,13 @@ __device__ __forceinline__ uint32_t block_size(uint32_t d, uint32_t B, bool &bad
 }
 
 // Decode table of one chunk: f:12 <<20 | (slot-cdf):12 <<8 | sym:8 (a7).
-// All 256 threads; returns false (uniformly) if the table is invalid.
-__device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red) {
+// All 256 threads; returns false (uniformly) if the table is invalid.  Every
+// thread fills its own 16 slots: mark each symbol's first slot, running max
+// over the thread's slots, block-wide exclusive max-scan -- balanced over the
+// warps (filling symbol by symbol left the warp owning the dominant exponents
+// with ~128 serial store iterations while the others waited at the barrier).
+// `scr`: 2 KiB of smem scratch (per-symbol f and cdf).
+__device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red, uint32_t *scr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const uint32_t f = ld_cg_u16(ft + tid);
   uint32_t incl = f;
@@ -42,12 +47,48 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
   __syncthreads();
   if (fsum != kM || bad) return false;
   const uint32_t cdf = woff + incl - f;
-  for (int k = 0; k < 32; ++k) {
-    const uint32_t fk = __shfl_sync(0xFFFFFFFFu, f, k);
-    const uint32_t ck = __shfl_sync(0xFFFFFFFFu, cdf, k);
-    const uint32_t sk = (uint32_t)(warp * 32 + k);
-    for (uint32_t t = lane; t < fk; t += 32) dtab[ck + t] = (fk << 20) | (t << 8) | sk;
+  scr[tid] = f;
+  scr[256 + tid] = cdf;
+  uint4 *d4 = reinterpret_cast<uint4 *>(dtab) + 4 * tid;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  dtab[cdf] = (uint32_t)tid;  // distinct first slots (every f >= 1)
+  __syncthreads();
+  uint32_t v[16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 q = d4[i];
+    v[4 * i] = q.x;
+    v[4 * i + 1] = q.y;
+    v[4 * i + 2] = q.z;
+    v[4 * i + 3] = q.w;
   }
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = m = max(m, v[i]);
+  uint32_t inc = m;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc = max(inc, tt);
+  }
+  if (lane == 31) s_red[warp] = inc;
+  __syncthreads();
+  uint32_t pre = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+  if (lane == 0) pre = 0;
+  for (int w = 0; w < warp; ++w) pre = max(pre, s_red[w]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t e[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t sym = max(pre, v[4 * i + k]);
+      const uint32_t slot = 16u * tid + 4 * i + k;
+      e[k] = (scr[sym] << 20) | ((slot - scr[256 + sym]) << 8) | sym;
+    }
+    d4[i] = make_uint4(e[0], e[1], e[2], e[3]);
+  }
+  __syncthreads();  // s_red and scr are free again
   return true;
 }
 

@@ -64,6 +64,7 @@ struct uzip_comm {
   cudaStream_t side;               // private stream for host reads (async error, stats)
   uzip_stats_t last;
   int nested;                      // inside uzip_allreduce: phases accumulate stats
+  uint32_t call_rounds;            // fused launches issued by the current call
 };
 
 namespace {
@@ -154,12 +155,13 @@ uint64_t round_elems(uzip_comm *c, int dt, bool compressed, uint64_t count, Stre
     return t.total(t.n_blocks * (uint64_t)t.B) <= c->L.slot_bytes && t.n_tiles() + 1 <= c->L.max_tiles &&
            t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_blocks) <= c->ws_job_bytes;
   };
-  // whole table chunks when one fits a slot, else whole tiles (a round shorter than a chunk has one chunk)
+  // whole table chunks when one fits a slot and the pipe chunk, else whole tiles (a round shorter
+  // than a chunk has one chunk)
   const uint64_t ge = group_elems(dt);  // rounds split at symbol-group boundaries
   uint64_t unit = (g.global ? (uint64_t)g.B * kTileBlocks : (uint64_t)g.CB * g.B) * ge;
-  if (!fits(unit)) unit = (uint64_t)g.B * kTileBlocks * ge;
-  uint64_t lo = 1, hi = cap / unit + 1;
-  while (lo < hi) {  // largest k with k*unit fitting a slot and the workspace
+  if (unit > cap || !fits(unit)) unit = (uint64_t)g.B * kTileBlocks * ge;
+  uint64_t lo = 1, hi = std::max<uint64_t>(1, cap / unit);
+  while (lo < hi) {  // largest k <= cap / unit (at least 1) with k*unit fitting a slot and the workspace
     const uint64_t k = (lo + hi + 1) / 2;
     if (fits(k * unit)) lo = k;
     else hi = k - 1;
@@ -258,6 +260,32 @@ void fwd_setup(uzip_comm *c, Plan &p, int j, const std::vector<int> &dsts) {
 }
 
 uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
+  // From the third launch of a call on, a slot's credit comes from a consumer
+  // launch of this same call: wait for it in k_credit (one thread) instead of
+  // in every CTA of the fused kernel, which would hold SM slots the consumer
+  // may need when both share a GPU (a12).
+  if (c->call_rounds++ >= 2) {
+    CreditWait w;
+    memset(&w, 0, sizeof w);
+    for (int j = 0; j < p.ne; ++j)
+      for (uint32_t d = 0; d < p.e[j].nd; ++d)
+        if (p.e[j].credit[d] && p.e[j].epoch[d] > 2 && w.n < 2 * kMaxRanks) {
+          w.cr[w.n] = p.e[j].credit[d];
+          w.epoch[w.n++] = p.e[j].epoch[d];
+        }
+    for (int j = 0; j < p.nd_jobs; ++j)
+      for (uint32_t d = 0; d < p.d[j].nfwd; ++d)
+        if (p.d[j].fcredit[d] && p.d[j].fepoch[d] > 2 && w.n < 2 * kMaxRanks) {
+          w.cr[w.n] = p.d[j].fcredit[d];
+          w.epoch[w.n++] = p.d[j].fepoch[d];
+        }
+    if (w.n) {
+      w.err = p.err;
+      w.timeout_ns = p.timeout_ns;
+      if (launch_credit_wait(w, st) != cudaSuccess) return UZIP_ERR_CUDA;
+      p.credit_ready = 1;
+    }
+  }
   for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
   for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += p.d[j].ntiles;
   p.n_c_items = p.has_copy ? p.c.ntiles : 0;
@@ -283,6 +311,7 @@ uzip_status_t begin_call(uzip_comm *c, uint64_t egress_raw, bool compressed, cud
     c->last.raw_bytes += egress_raw;
     return UZIP_OK;
   }
+  c->call_rounds = 0;
   c->last.raw_bytes = egress_raw;
   c->last.compressed = compressed ? 1 : 0;
   c->last.wire_bytes = 0;

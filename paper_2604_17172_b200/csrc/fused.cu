@@ -23,7 +23,46 @@ cudaError_t preload_f32_red();
 cudaError_t preload_e4m3_enc();
 cudaError_t preload_e5m2_enc();
 
+// Wait (one thread) until every slot credit of the next fused launch has
+// arrived; on timeout record the error (site 4) -- the fused kernel then aborts
+// its encode / forward items instead of overwriting a slot still in use.
+__global__ void k_credit(const CreditWait w) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0 = 0;
+  for (uint32_t i = 0; i < w.n; ++i) {
+    for (int spin = 0;; ++spin) {
+      const unsigned long long v = ld_acquire_sys_u64(w.cr[i]);
+      if (v >= (unsigned long long)(w.epoch[i] - 2)) break;
+      if ((spin & 63) == 63) {
+        if (ld_volatile_u32(w.err)) return;
+        const unsigned long long now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > w.timeout_ns) {
+          if (atomicCAS(w.err, 0u, (uint32_t)UZIP_ERR_TIMEOUT) == 0u) {
+            w.err[1] = 4;
+            w.err[2] = w.epoch[i];
+            w.err[3] = (uint32_t)(v >> 32);
+            w.err[4] = (uint32_t)v;
+            w.err[5] = (uint32_t)(uintptr_t)w.cr[i];
+            w.err[6] = 0;
+            __threadfence_system();
+          }
+          return;
+        }
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+cudaError_t launch_credit_wait(const CreditWait &w, cudaStream_t st) {
+  k_credit<<<1, 32, 0, st>>>(w);
+  return cudaGetLastError();
+}
+
 cudaError_t preload_kernels() {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, k_credit) != cudaSuccess) return cudaGetLastError();
   cudaError_t (*fns[])() = {preload_bf16_enc, preload_bf16_red, preload_f16_enc, preload_f16_red,
                             preload_f32_enc,  preload_f32_red,  preload_e4m3_enc, preload_e5m2_enc};
   for (auto f : fns) {

@@ -624,7 +624,9 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
     if (tid == 0) {
       uint32_t ok = 1;
-      for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
+      if (P.credit_ready) ok = ld_volatile_u32(P.err) == 0;  // k_credit waited (or failed)
+      else
+        for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
       S.abort = ok ? 0u : 1u;
     }
     __syncthreads();
@@ -900,7 +902,9 @@ static __device__ void forward_tile(const Plan &P, const DecJob &J, uint64_t t, 
   if (!((fwd_done >> jidx) & 1u)) {  // first forward of this job in this CTA: the hops' slots are free
     if (tid == 0) {
       uint32_t ok = 1;
-      for (uint32_t d = 0; d < J.nfwd && ok; ++d) ok = wait_credit(P, J.fcredit[d], J.fepoch[d]);
+      if (P.credit_ready) ok = ld_volatile_u32(P.err) == 0;
+      else
+        for (uint32_t d = 0; d < J.nfwd && ok; ++d) ok = wait_credit(P, J.fcredit[d], J.fepoch[d]);
       S.abort = ok ? 0u : 1u;
     }
     __syncthreads();
@@ -980,7 +984,8 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
   }
   uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + P.ring_bytes);
   if (g.n_blocks && need_table) {
-    if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
+    if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red,
+                    reinterpret_cast<uint32_t *>(smem + C::kEncTab))) {
       if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
       dec_key = ~0ull;
       return;
@@ -1114,7 +1119,8 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     if (S.abort) return;
     const uint8_t *stream = J.src[s];
     if (g.n_blocks && need_table) {
-      if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red)) {
+      if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red,
+                    reinterpret_cast<uint32_t *>(smem + C::kEncTab))) {
         if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
         dec_key = ~0ull;
         return;

@@ -90,6 +90,20 @@ struct Plan {
   uint64_t timeout_ns;
   int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
   uint32_t stress;                          // debug: != 0 injects pseudo-random delays (UZIP_STRESS)
+  uint32_t credit_ready;                    // 1: k_credit already waited for every slot credit of this launch
+};
+
+// Slot credits one launch needs (a12), waited for by k_credit -- one thread --
+// before the fused kernel starts, so its CTAs never hold SM slots while the
+// consumer that releases the credit still needs them (loopback, co-scheduled
+// compute).
+struct CreditWait {
+  const unsigned long long *cr[2 * kMaxRanks];
+  uint32_t epoch[2 * kMaxRanks];
+  uint32_t n;
+  uint32_t stress;
+  uint32_t *err;
+  uint64_t timeout_ns;
 };
 
 // k_hist splits a chunk's sample over up to kMaxHistParts CTAs of >= 16 Ki symbols.
@@ -123,5 +137,6 @@ static_assert(sizeof(Plan) <= 30000, "kernel parameter space");
 cudaError_t launch_tables(int dtype, const Plan &p, cudaStream_t st);
 cudaError_t preload_kernels();  // per device: defeat lazy loading for spin-waiting kernels
 cudaError_t launch_fused(int dtype, const Plan &p, cudaStream_t st, int max_ctas);
+cudaError_t launch_credit_wait(const CreditWait &w, cudaStream_t st);
 
 }  // namespace uzip

@@ -1,0 +1,134 @@
+"""Ablations of the fused P2P design on one B200.
+
+    python scripts/ablations.py [--bytes N] [--steps K] [--out FILE]
+
+All legs move the same 1 GiB bf16 N(0, 0.02) tensor from loopback rank 0 to rank 1 (both ranks on this
+one GPU, so sender and receiver share SMs and HBM -- a lower bound for the NVLink case) and check the
+bytes:
+  * fused           uzip_send / uzip_recv, default configuration (one persistent kernel per side per
+                    256 MiB round, tile-granular overlap);
+  * chunked_8MiB    the same calls with pipe_chunk_bytes = 8 MiB: one UZB1 stream and one launch per 8 MiB
+                    chunk -- the paper's "8 MB chunked pipeline" / NCCL-slice granularity;
+  * chunked_1MiB    the same at 1 MiB;
+  * encode_send     uzip_compress of the whole message, a device copy of the stream (the wire), then
+                    uzip_decompress -- serial, no overlap (fig:compare_with_native_pipeline);
+  * sm_limited      the fused path with each side's kernel capped at max_ctas CTAs (fig:resource_usage;
+                    a CTA cap stands in for Green Contexts, f3).
+Timing: CUDA events on rank 0's stream around K steps after warm-up (inputs exceed L2).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+GB = 1e9
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bytes", type=int, default=1 << 30)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+    import paper_2604_17172_b200 as uz
+    uz.build()
+    n = args.bytes // 2
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    x = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    raw = 2 * n
+    res = {"workload": f"loopback P2P of {raw >> 20} MiB bf16 N(0,0.02) on one B200", "legs": {}}
+
+    def timed(step, s0):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s0)
+        for _ in range(args.steps):
+            step()
+        e1.record(s0)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    def p2p_leg(name, **cfg):
+        cfg.setdefault("staging_bytes", 1 << 30)
+        comms = uz.Comm.init_all(2, [0, 0], **cfg)
+        s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+        y.zero_()
+
+        threaded = "pipe_chunk_bytes" in cfg
+
+        def step():
+            s1.wait_stream(s0)
+            if threaded:  # each side from its own thread, as two processes would: hundreds of small rounds
+                th = [threading.Thread(target=comms[0].send, args=(x, 1, s0)),  # can fill one thread's
+                      threading.Thread(target=comms[1].recv, args=(y, 0, s1))]  # launch queue first
+                for t in th:
+                    t.start()
+                for t in th:
+                    t.join()
+            else:
+                comms[0].send(x, 1, s0)
+                comms[1].recv(y, 0, s1)
+            s0.wait_stream(s1)
+
+        ms = timed(step, s0)
+        ok = torch.equal(x.view(torch.int16), y.view(torch.int16)) and [c.async_error() for c in comms] == [0, 0]
+        st = comms[0].stats()
+        for c in comms:
+            c.destroy()
+        res["legs"][name] = {"GBps": round(raw / (ms / 1e3) / GB, 2), "ms": round(ms, 4), "bit_exact": bool(ok),
+                             "wire_ratio": round(st["wire_bytes"] / max(1, st["raw_bytes"]), 5),
+                             "config": {k: v for k, v in cfg.items() if k != "staging_bytes"}}
+        print(name, res["legs"][name], flush=True)
+
+    p2p_leg("fused", max_ctas=2 * 148)
+    p2p_leg("chunked_8MiB", max_ctas=2 * 148, pipe_chunk_bytes=8 << 20)
+    p2p_leg("chunked_1MiB", max_ctas=2 * 148, pipe_chunk_bytes=1 << 20)
+    for m in (16, 37, 74, 148):
+        p2p_leg(f"sm_limited_{m}ctas", max_ctas=m)
+
+    # encode-send: compress, copy the stream (the wire), decompress; serial
+    stream = torch.cuda.Stream()
+    cap = uz.compress_bound(n, uz.BF16)
+    sbuf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    rbuf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = uz.Workspace(0).get(uz.workspace_bytes(n, uz.BF16), stream)
+    with torch.cuda.stream(stream):
+        uz.compress(x, out=sbuf, out_bytes=nb, stream=stream, ws=ws)
+    torch.cuda.synchronize()
+    wire = int(nb.item())
+    y.zero_()
+
+    def es_step():
+        with torch.cuda.stream(stream):
+            uz.compress(x, out=sbuf, out_bytes=nb, stream=stream, ws=ws)
+            rbuf[:wire].copy_(sbuf[:wire])
+            uz.decompress(rbuf, n, uz.BF16, out=y, status=st, stream=stream, ws=ws, in_bytes=wire)
+
+    ms = timed(es_step, stream)
+    ok = int(st.item()) == 0 and torch.equal(x.view(torch.int16), y.view(torch.int16))
+    res["legs"]["encode_send"] = {"GBps": round(raw / (ms / 1e3) / GB, 2), "ms": round(ms, 4), "bit_exact": bool(ok),
+                                  "wire_ratio": round(wire / raw, 5),
+                                  "note": "uzip_compress + device copy of the stream + uzip_decompress, serial"}
+    print("encode_send", res["legs"]["encode_send"], flush=True)
+    line = json.dumps(res)
+    print(line)
+    if args.out:
+        open(args.out, "w").write(line + "\n")
+
+
+if __name__ == "__main__":
+    main()

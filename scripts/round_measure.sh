@@ -8,3 +8,5 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 600 python __graft_entry__.py > gpurun_out/smoke.log 2>&1
 ./scripts/ncu_codec.sh
 cat gpurun_out/bench_default.log gpurun_out/bench_reference.log gpurun_out/smoke.log
+timeout 600 python scripts/ablations.py --out gpurun_out/ablations.json > gpurun_out/ablations.log 2>&1
+tail -1 gpurun_out/ablations.log

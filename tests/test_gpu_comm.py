@@ -252,6 +252,45 @@ def test_reduce_rejects_unknown_op_and_fp8(uz):
         g.close()
 
 
+@pytest.mark.parametrize("pipe_mib", [16, 24])
+@pytest.mark.parametrize("issue", ["send_first", "threads"])
+def test_p2p_many_multichunk_rounds_no_starvation(uz, pipe_mib, issue):
+    """Dozens of 2-3-chunk rounds through 2 slots with sender and receiver sharing the GPU: the
+    credit for round k comes from the receiver's round k-2 of the same call.  Regression: when
+    every CTA of the sender's kernel spun on that credit, the receiver's kernel could not get SM
+    slots and both timed out (now k_credit waits, one thread, before the fused launch)."""
+    import threading
+    comms = uz.Comm.init_all(2, [0, 0], staging_bytes=1 << 30, max_ctas=296, pipe_chunk_bytes=pipe_mib << 20,
+                             poll_timeout_ms=5000)
+    try:
+        n = 384 << 20  # 768 MiB bf16: 48 (16 MiB) or 32 (24 MiB) rounds of 2-3 table chunks
+        g = torch.Generator(device="cuda")
+        g.manual_seed(pipe_mib)
+        x = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+        y = torch.empty_like(x)
+        s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+        for _ in range(2):
+            y.zero_()
+            torch.cuda.synchronize()
+            snd = lambda: comms[0].send(x, 1, s0)  # noqa: E731
+            rcv = lambda: comms[1].recv(y, 0, s1)  # noqa: E731
+            if issue == "send_first":
+                snd()
+                rcv()
+            else:
+                th = [threading.Thread(target=snd), threading.Thread(target=rcv)]
+                for t in th:
+                    t.start()
+                for t in th:
+                    t.join()
+            torch.cuda.synchronize()
+            assert [c.async_error() for c in comms] == [0, 0], [c.error_detail() for c in comms]
+            assert torch.equal(x.view(torch.int16), y.view(torch.int16))
+    finally:
+        for c in comms:
+            c.destroy()
+
+
 def test_reduce_scatter_rejects_unaligned_shards(uz):
     g = Group(uz, 2, **CFG_SMALL)
     try:
