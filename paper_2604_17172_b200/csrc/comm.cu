@@ -65,6 +65,7 @@ struct uzip_comm {
   uzip_stats_t last;
   int nested;                      // inside uzip_allreduce: phases accumulate stats
   uint32_t call_rounds;            // fused launches issued by the current call
+  float *acc;                      // reduce accumulators (allocated by the first reduce call)
 };
 
 namespace {
@@ -132,6 +133,7 @@ void free_comm(uzip_comm *c) {
       if (p != c->rank && c->peer[p]) cudaIpcCloseMemHandle(c->peer[p]);
   if (c->region) cudaFree(c->region);
   if (c->ws) cudaFree(c->ws);
+  if (c->acc) cudaFree(c->acc);
   if (c->side) cudaStreamDestroy(c->side);
   c->magic = 0;
   delete c;
@@ -176,6 +178,7 @@ void base_plan(uzip_comm *c, Plan &p, int dt) {
   p.dtype = dt;
   p.ticket = ws_ticket(c);
   p.err = reinterpret_cast<uint32_t *>(c->region);
+  p.acc = c->acc;
   p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
   static const uint32_t stress = (uint32_t)strtoul(getenv("UZIP_STRESS") ? getenv("UZIP_STRESS") : "0", nullptr, 0);
   p.stress = stress;
@@ -317,6 +320,16 @@ uzip_status_t begin_call(uzip_comm *c, uint64_t egress_raw, bool compressed, cud
   c->last.wire_bytes = 0;
   if (cudaMemsetAsync(ws_wire(c), 0, 8, st) != cudaSuccess) return UZIP_ERR_CUDA;
   return UZIP_OK;
+}
+
+// fp32 accumulators of the reduce kernel: B (<= 4096) floats per warp of every
+// CTA the largest grid can hold (4 per SM bounds the reduce kernel's occupancy).
+uzip_status_t ensure_acc(uzip_comm *c) {
+  if (c->acc) return UZIP_OK;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) return UZIP_ERR_CUDA;
+  const size_t bytes = (size_t)sms * 4 * kWarps * kMaxB * sizeof(float);
+  return cudaMalloc(&c->acc, bytes) == cudaSuccess ? UZIP_OK : UZIP_ERR_CUDA;
 }
 
 uzip_status_t check_dtype(uzip_dtype_t dt) {
@@ -526,6 +539,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
   const bool comp = compress_message(c, msg);
   cudaStream_t st = (cudaStream_t)stream;
   if (uzip_status_t s = begin_call(c, (uint64_t)(N - 1) * recvcount * eb, comp, st)) return s;
+  if (uzip_status_t s = ensure_acc(c)) return s;
   const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
   uint8_t *out = static_cast<uint8_t *>(recvbuf);
   const uint64_t per = round_elems(c, dt, comp, recvcount, nullptr);

@@ -34,6 +34,9 @@
 #ifndef UZIP_ENC_GROUP
 #define UZIP_ENC_GROUP 8  // encoder rounds whose symbols/table entries are loaded ahead
 #endif
+#ifndef UZIP_RED_MINB
+#define UZIP_RED_MINB 3   // resident CTAs per SM targeted by reduce launches (accumulators in L2, not smem)
+#endif
 #ifndef UZIP_ENC_MINB
 #define UZIP_ENC_MINB 3   // resident CTAs per SM targeted by launches with encode items (measured)
 #endif
@@ -353,11 +356,9 @@ struct FusedCfg {
   static constexpr int kEncTab = 4096;                      // 256 x uint4
   static constexpr int kWarpBuf = B + 256;                  // per warp: symbols/words (E) or payload + ring (D)
   static constexpr int kDecTab = 4096 * 4;
-  static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce)
-  static constexpr int ring(bool red) { return red ? 0 : 16384; }  // coded tile awaiting its offset
-  static constexpr int smem(bool dec, bool red) {
-    return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0) + (red ? kWarps * kAcc : 0);
-  }
+  static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce; in P.acc)
+  static constexpr int ring(bool) { return 16384; }         // coded tile awaiting its offset
+  static constexpr int smem(bool dec, bool red) { return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0); }
 };
 
 struct FusedShared {
@@ -1019,6 +1020,20 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
   dec_done(J);
 }
 
+// The warp's fp32 accumulator lives in global memory (P.acc, B floats per
+// (CTA, warp), L2-resident): every lane reads and writes only its own 8-element
+// groups, the same ones for every source, so it is thread-private data moved
+// with 128-bit accesses.  In smem it would take 128 KiB per CTA and hold the
+// reduce kernel to one CTA per SM.
+__device__ __forceinline__ void acc_load8(const float *p, float *v) {
+  const float4 a = *reinterpret_cast<const float4 *>(p), b = *reinterpret_cast<const float4 *>(p + 4);
+  v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+}
+__device__ __forceinline__ void acc_store8(float *p, const float *v) {
+  *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4 *>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
 // Epilogue that folds a decoded source into the warp's fp32 accumulator (a9).
 struct FoldEpi {
   float *acc;
@@ -1027,17 +1042,14 @@ struct FoldEpi {
   template <int DT>
   __device__ __forceinline__ void apply(uint32_t e0, uint4 a, uint4 b) const {
     float v[8];
-    if (!first)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = acc[e0 + i];
+    if (!first) acc_load8(acc + e0, v);
     if (DT == kF32) {
       fold_vec<DT>(v, a, first, op);
       fold_vec<DT>(v + 4, b, first, op);
     } else {
       fold_vec<DT>(v, a, first, op);
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[e0 + i] = v[i];
+    acc_store8(acc + e0, v);
   }
 };
 
@@ -1049,7 +1061,6 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const StreamGeom &g = J.g;
   const uint32_t eb = elem_bytes(DT);
-  constexpr int kPer = C::kVec;
 
   if (J.raw) {  // ---- below the threshold: fold raw tiles
     for (uint32_t s = 0; s < J.nsrc; ++s) {
@@ -1091,7 +1102,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
   const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
   const uint64_t b = b0 + warp;
   uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true));
-  float *acc = reinterpret_cast<float *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true) + C::kDecTab) + warp * B;
+  float *acc = P.acc + ((uint64_t)blockIdx.x * kWarps + warp) * B;
   uint8_t *pay = smem + C::kEncTab + warp * C::kWarpBuf;
   uint8_t *symb = pay + B;
   bool bad = false;
@@ -1101,12 +1112,14 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     if ((int32_t)s == J.me) {  // own shard: never compressed
       if (b < g.n_blocks) {
         const uint8_t *src = J.src[s] + b * (uint64_t)B * eb;
-        for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer) {
+        // the same lane-to-element map as the decode epilogue (8 consecutive elements per lane
+        // and group), so each accumulator element stays with one thread
+        for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
           float a[8];
-          if (!first)
-            for (int i = 0; i < kPer; ++i) a[i] = acc[e + i];
+          if (!first) acc_load8(acc + e, a);
           fold_vec<DT>(a, ldg_nc_v4(src + e * eb), first, J.op);
-          for (int i = 0; i < kPer; ++i) acc[e + i] = a[i];
+          if (DT == kF32) fold_vec<DT>(a + 4, ldg_nc_v4(src + e * eb + 16), first, J.op);
+          acc_store8(acc + e, a);
         }
       }
       __syncwarp();
@@ -1168,8 +1181,12 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
   if (bad && lane == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
   if (b < g.n_blocks) {  // one rounding to the dtype, 128-bit stores
     uint8_t *dst = J.out + b * (uint64_t)B * eb;
-    for (uint32_t e = lane * kPer; e < (uint32_t)B; e += 32 * kPer)
-      *reinterpret_cast<uint4 *>(dst + e * eb) = narrow_vec<DT>(acc + e);
+    for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
+      float a[8];
+      acc_load8(acc + e, a);
+      *reinterpret_cast<uint4 *>(dst + e * eb) = narrow_vec<DT>(a);
+      if (DT == kF32) *reinterpret_cast<uint4 *>(dst + e * eb + 16) = narrow_vec<DT>(a + 4);
+    }
   }
   __syncthreads();
   if (t == J.ntiles - 1) {  // raw tails of every source, folded in rank order
@@ -1286,8 +1303,7 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   const bool dec = p.n_d_items > 0;
   // the ring parks coded tiles (encode launches only; none in the reduce variant)
   p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
-  const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0) +
-                   (RED ? kWarps * C::kAcc : 0);
+  const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0);
   auto kern = k_fused<DT, B, RED, MINB>;
   static int attr_set = 0;
   if (attr_set < C::smem(true, RED)) {
@@ -1308,7 +1324,7 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
 template <int DT, int B, bool RED>
 cudaError_t launch_fused_t(const Plan &p, cudaStream_t st, int max_ctas) {
   if constexpr (RED) {
-    return launch_fused_k<DT, B, RED, 1>(p, st, max_ctas);
+    return launch_fused_k<DT, B, RED, UZIP_RED_MINB>(p, st, max_ctas);
   } else {
     if (p.n_e_items > 0) return launch_fused_k<DT, B, RED, UZIP_ENC_MINB>(p, st, max_ctas);
     return launch_fused_k<DT, B, RED, 4>(p, st, max_ctas);
@@ -1325,9 +1341,9 @@ cudaError_t preload_t() {
   cudaFuncAttributes a;
   cudaError_t e = cudaSuccess;
   if constexpr (RED) {
-    e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, true, 1>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, true, 1>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, true, 1>);
+    e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, true, UZIP_RED_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, true, UZIP_RED_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, true, UZIP_RED_MINB>);
   } else {
     e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_ENC_MINB>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_ENC_MINB>);

@@ -91,6 +91,7 @@ struct Plan {
   int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
   uint32_t stress;                          // debug: != 0 injects pseudo-random delays (UZIP_STRESS)
   uint32_t credit_ready;                    // 1: k_credit already waited for every slot credit of this launch
+  float *acc;                               // reduce: fp32 accumulators, B floats per (CTA, warp) (L2-resident)
 };
 
 // Slot credits one launch needs (a12), waited for by k_credit -- one thread --

@@ -17,12 +17,13 @@ def main():
     ap.add_argument("--n", type=int, default=4)
     ap.add_argument("--mib", type=int, default=256)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--ctas_per_sm", type=int, default=1, help="total CTAs = 148 x this, split over the ranks")
     args = ap.parse_args()
     import torch
     import paper_2604_17172_b200 as uz
     uz.build()
     N = args.n
-    comms = uz.Comm.init_all(N, [0] * N, max_ctas=148 // N, staging_bytes=1 << 30)
+    comms = uz.Comm.init_all(N, [0] * N, max_ctas=148 * args.ctas_per_sm // N, staging_bytes=1 << 30)
     streams = [torch.cuda.Stream() for _ in range(N)]
     numel = (args.mib << 20) // 2
     g = torch.Generator(device="cuda")
