@@ -65,6 +65,7 @@ struct uzip_comm {
   uzip_stats_t last;
   int nested;                      // inside uzip_allreduce: phases accumulate stats
   uint32_t call_rounds;            // fused launches issued by the current call
+  uint32_t share;                  // ranks (incl. this one) whose kernels run on this same GPU
   float *acc;                      // reduce accumulators (allocated by the first reduce call)
 };
 
@@ -182,6 +183,7 @@ void base_plan(uzip_comm *c, Plan &p, int dt) {
   p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
   static const uint32_t stress = (uint32_t)strtoul(getenv("UZIP_STRESS") ? getenv("UZIP_STRESS") : "0", nullptr, 0);
   p.stress = stress;
+  p.share = c->share ? c->share : 1;
 }
 
 // Encode job of `n` elements at `in` (round stream) into destinations dsts.
@@ -361,6 +363,7 @@ uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_d
     cudaIpcMemHandle_t h;
     uint64_t total, slot, max_tiles;
     int32_t device, rank;
+    unsigned char uuid[16];  // which physical GPU: co-located ranks share its SMs
   } mine, all[kMaxRanks];
   memset(&mine, 0, sizeof mine);
   if (cudaIpcGetMemHandle(&mine.h, c->region) != cudaSuccess) {
@@ -372,6 +375,10 @@ uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_d
   mine.max_tiles = c->L.max_tiles;
   mine.device = cuda_device;
   mine.rank = rank;
+  {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cuda_device) == cudaSuccess) memcpy(mine.uuid, prop.uuid.bytes, 16);
+  }
   if (bootstrap(&mine, all, sizeof(Card), ctx) != 0) {
     free_comm(c);
     return UZIP_ERR_COMM;
@@ -381,6 +388,7 @@ uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_d
       free_comm(c);
       return UZIP_ERR_COMM;  // every rank must use the same configuration
     }
+    if (memcmp(all[p].uuid, mine.uuid, 16) == 0) ++c->share;
     if (p == rank) {
       c->peer[p] = c->region;
       continue;
@@ -428,7 +436,11 @@ uzip_status_t uzip_comm_init_all(uzip_comm_t *comms, int nranks, const int *devi
       }
     }
   }
-  for (int r = 0; r < nranks; ++r) comms[r] = cs[r];
+  for (int r = 0; r < nranks; ++r) {
+    cs[r]->share = 0;
+    for (int p = 0; p < nranks; ++p) cs[r]->share += devices[p] == devices[r];
+    comms[r] = cs[r];
+  }
   return UZIP_OK;
 }
 

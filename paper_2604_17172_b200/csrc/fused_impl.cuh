@@ -1316,6 +1316,11 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   const uint64_t items = p.n_e_items + p.n_c_items + p.n_d_items;
   int grid = sm_count() * occ;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  // Ranks sharing this GPU (loopback): a launch whose decode items spin on a
+  // peer's flags may hold at most 1/share of the slots, so the peer's kernels
+  // (the producers it waits for) always find an SM.
+  if (p.share > 1 && p.n_d_items > 0 && grid > sm_count() * occ / (int)p.share)
+    grid = sm_count() * occ / (int)p.share > 0 ? sm_count() * occ / (int)p.share : 1;
   if ((uint64_t)grid > items) grid = (int)(items ? items : 1);
   kern<<<grid, 256, smem, st>>>(p);
   return cudaGetLastError();

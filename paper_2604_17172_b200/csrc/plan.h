@@ -91,6 +91,7 @@ struct Plan {
   int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
   uint32_t stress;                          // debug: != 0 injects pseudo-random delays (UZIP_STRESS)
   uint32_t credit_ready;                    // 1: k_credit already waited for every slot credit of this launch
+  uint32_t share;                           // ranks whose kernels share this GPU (loopback / co-located processes)
   float *acc;                               // reduce: fp32 accumulators, B floats per (CTA, warp) (L2-resident)
 };
 
