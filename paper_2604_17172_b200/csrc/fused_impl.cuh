@@ -32,7 +32,7 @@
 
 // Tuning knobs (defaults measured best on B200; overridable for experiments with -D)
 #ifndef UZIP_ENC_GROUP
-#define UZIP_ENC_GROUP 8  // encoder rounds whose symbols/table entries are loaded ahead
+#define UZIP_ENC_GROUP 4  // encoder rounds whose symbols/table entries are loaded ahead
 #endif
 #ifndef UZIP_RED_MINB
 #define UZIP_RED_MINB 3   // resident CTAs per SM targeted by reduce launches (accumulators in L2, not smem)
@@ -511,6 +511,12 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
   uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
   uint32_t x = kL, wp = 0;
   bool over = false;
+  // Deferred word store (buf path): round u's word is stored during round u+1, so the store's
+  // index (ballot -> popc) and its data register have a round of slack -- stored in place, the
+  // store waited on the popc and the shift of x waited for the store to read x (ncu: the two
+  // largest short_scoreboard stalls of the round loop).
+  uint32_t dw = 0, didx = 0;
+  bool dp = false;
   constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
   constexpr int kG = UZIP_ENC_GROUP;
 #pragma unroll 1
@@ -530,8 +536,9 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
         if (p && idx + 1 < kCap)
           for (uint32_t d = 0; d < J.nd; ++d)
             *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + 2 * idx) = (uint16_t)x;
-      } else if (p) {
-        buf16[idx] = (uint16_t)x;
+      } else {
+        if (dp) buf16[didx] = (uint16_t)dw;
+        dp = p, dw = x, didx = idx;
       }
       x = p ? (x >> 16) : x;
       wp += __popc(m);
@@ -540,6 +547,7 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
     }
     over |= wp > lim;
   }
+  if (!GLOBAL && dp) buf16[didx] = (uint16_t)dw;
   x_out = x;
   K = wp;
   ovf = over;
