@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-loopback", action="store_true", help="skip the loopback P2P context field (e.g. under ncu)")
+    ap.add_argument("--no-dtypes", action="store_true", help="skip the per-dtype U[-1,1] context field (e.g. under ncu)")
     return ap.parse_args()
 
 
@@ -250,7 +251,7 @@ def run_codec(args):
     if not args.no_e2e:
         e2e = run_codec_e2e(uz, x, args, stream)
     loop = None if args.no_loopback else run_loopback_p2p(uz, x, args)
-    per_dtype = run_per_dtype(uz, args)
+    per_dtype = None if args.no_dtypes else run_per_dtype(uz, args)
 
     line = {
         "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",
