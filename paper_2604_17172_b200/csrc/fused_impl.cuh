@@ -515,8 +515,11 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
   // index (ballot -> popc) and its data register have a round of slack -- stored in place, the
   // store waited on the popc and the shift of x waited for the store to read x (ncu: the two
   // largest short_scoreboard stalls of the round loop).
-  uint32_t dw = 0, didx = 0;
-  bool dp = false;
+  // Every lane stores every round: a lane without a word writes to its own spare slot past the
+  // B-byte buffer (words B/2 + lane, inside the warp's B + 256 bytes), so the store needs no
+  // predicate carried into the next round.
+  const uint32_t spare = (uint32_t)B / 2 + (uint32_t)lane;
+  uint32_t dw = 0, didx = spare;
   constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
   constexpr int kG = UZIP_ENC_GROUP;
 #pragma unroll 1
@@ -537,8 +540,8 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
           for (uint32_t d = 0; d < J.nd; ++d)
             *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + 2 * idx) = (uint16_t)x;
       } else {
-        if (dp) buf16[didx] = (uint16_t)dw;
-        dp = p, dw = x, didx = idx;
+        buf16[didx] = (uint16_t)dw;
+        dw = x, didx = p ? idx : spare;
       }
       x = p ? (x >> 16) : x;
       wp += __popc(m);
@@ -547,7 +550,7 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
     }
     over |= wp > lim;
   }
-  if (!GLOBAL && dp) buf16[didx] = (uint16_t)dw;
+  if (!GLOBAL) buf16[didx] = (uint16_t)dw;
   x_out = x;
   K = wp;
   ovf = over;
