@@ -15,12 +15,29 @@
 namespace uzip {
 
 // ================================================================ k_decode
+// Occupancy (the decoder is latency-bound on the table-lookup -> ALU -> word-fetch chain, so
+// resident warps matter): a coded block is staged in smem only up to kStage bytes -- every
+// realistic block is far below it (bf16 weights ~1.4 KB, f16 uniform ~2.8 KB) -- and a larger
+// one (rare) or a raw block is decoded / joined straight from global memory.  With kStage =
+// 3200 and 256-block segments a CTA needs 44 KB, so 5 CTAs (40 warps) fit per SM instead of 4.
+#ifndef UZIP_DEC_MINB
+#define UZIP_DEC_MINB 5
+#endif
+#ifndef UZIP_DEC_STAGE
+#define UZIP_DEC_STAGE 3200
+#endif
+#ifndef UZIP_DEC_SEG
+#define UZIP_DEC_SEG 256
+#endif
 struct DecShared {
-  static constexpr int kTab = 4096 * 4;          // decode table
-  static constexpr int kOff = 1024 * 4;          // per-segment block offsets (relative to chunk)
-  static constexpr int kWarpBuf = kMaxB + 256;   // staged payload + 8-round symbol ring
+  static constexpr int kTab = 4096 * 4;              // decode table
+  static constexpr int kSeg = UZIP_DEC_SEG;          // blocks per segment (a multiple of 256)
+  static constexpr int kOff = kSeg * 4;              // per-segment block offsets (relative to chunk)
+  static constexpr int kStage = UZIP_DEC_STAGE;      // staged payload bytes per warp (multiple of 16)
+  static constexpr int kWarpBuf = kStage + 256;      // staged payload + 8-round symbol ring
   static constexpr int kBytes = kTab + kOff + kWarps * kWarpBuf;
 };
+static_assert(DecShared::kStage % 16 == 0 && DecShared::kSeg % 256 == 0, "decoder smem layout");
 
 __device__ __forceinline__ void set_err(CodecWs &ws, uint32_t code) { atomicCAS(ws.err, 0u, code); }
 
@@ -32,15 +49,21 @@ __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom 
                                uint8_t *ring, uint8_t *__restrict__ out, CodecWs &ws) {
   const int lane = threadIdx.x & 31;
   const uint8_t *src = in + g.off_pay + off;
-  uint4 *dstv = reinterpret_cast<uint4 *>(pay);
-  for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = ld_cg_v4(src + 16 * i);
-  __syncwarp();
   uint8_t *dst = out + b * (uint64_t)B * g.eb;
+  bool ok = true;
   if (d == kRawBlock) {
-    join_block<DT, B>(pay, in, g, b, dst);
-  } else if (!decode_join_warp<DT, B>(pay, d, dtab, ring, in, g, b, dst)) {
-    if (lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
+    join_block<DT, B>(src, in, g, b, dst);  // raw symbols joined straight from the stream
+  } else if (size <= (uint32_t)DecShared::kStage) {
+    uint4 *dstv = reinterpret_cast<uint4 *>(pay);
+    for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = ld_cg_v4(src + 16 * i);
+    __syncwarp();
+    ok = decode_join_warp<DT, B>(pay, d, dtab, ring, in, g, b, dst);
+  } else {
+    // rare: a coded block larger than the staging area is decoded in place from global memory
+    // (word indices never leave [0, K), so even a corrupt stream is read in bounds)
+    ok = decode_join_warp<DT, B>(src, d, dtab, ring, in, g, b, dst);
   }
+  if (!ok && lane == 0) set_err(ws, UZIP_ERR_CORRUPT_STREAM);
   __syncwarp();
 }
 
@@ -63,7 +86,7 @@ __device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256, 4) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
+__global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
                                                   uint8_t *__restrict__ out, uint64_t n, CodecWs ws,
                                                   int32_t *__restrict__ d_status) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -71,7 +94,7 @@ __global__ void __launch_bounds__(256, 4) k_decode(const uint8_t *__restrict__ i
   uint32_t *soff = reinterpret_cast<uint32_t *>(smem + DecShared::kTab);
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   uint8_t *pay = smem + DecShared::kTab + DecShared::kOff + warp * DecShared::kWarpBuf;
-  uint8_t *ring = pay + kMaxB;
+  uint8_t *ring = pay + DecShared::kStage;
 
   __shared__ uint32_t s_red[kWarps];
   __shared__ uint32_t s_bad;
@@ -192,8 +215,8 @@ __global__ void __launch_bounds__(256, 4) k_decode(const uint8_t *__restrict__ i
       }
       const unsigned long long cbase = coff[c];
       // ---- segments of <= 1024 blocks: exclusive scan of sizes, then decode
-      for (uint64_t seg = s0; seg < chunk_stop; seg += 1024) {
-        const uint64_t seg_end = min(chunk_stop, seg + 1024);
+      for (uint64_t seg = s0; seg < chunk_stop; seg += DecShared::kSeg) {
+        const uint64_t seg_end = min(chunk_stop, seg + (uint64_t)DecShared::kSeg);
         const unsigned long long run0 = s_base;
         unsigned long long run = run0;
         for (uint64_t bb0 = seg; bb0 < seg_end; bb0 += 256) {

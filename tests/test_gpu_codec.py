@@ -240,6 +240,26 @@ def test_encoder_word_overflow_rare_path(uz, orc, dtype):
 
 
 
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+def test_large_coded_blocks_decoded_in_place(uz, orc, dtype):
+    """Blocks that compress only a little (exponent symbols uniform over 128 values, ~7.1 bits
+    each): their coded size (~3.7 KB of 4 KB) exceeds the decoder's 3200-byte smem staging area,
+    so k_decode reads them in place from global memory.  Stream == oracle, round trip exact."""
+    B, nb = 4096, 10
+    bits = synth.random_bits(nb * B + 5, 91, dtype).copy()
+    top = {BF16: 1 << 14, F16: 1 << 15, F32: 1 << 30}[dtype]  # the symbol's most significant bit
+    bits &= ~np.array(top, dtype=bits.dtype)
+    ref = orc.compress(dtype, bits)
+    raw = bits.size * bits.itemsize
+    # coded, not stored raw: between residual + 3200 B and residual + B per block
+    res = {BF16: 0.5, F16: 0.5, F32: 0.75}[dtype]
+    assert res + 3200 / (B * bits.itemsize) < len(ref) / raw < res + 1 / bits.itemsize - 0.005
+    got = gpu_compress(uz, bits, dtype)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, bits.size, dtype)
+    assert st == 0 and np.array_equal(back, bits)
+
+
 FP8_GENS = {
     "U": lambda n, s, d: synth.uniform(n, s, d),
     "W": lambda n, s, d: synth.normal(n, 0.02, s, d),
