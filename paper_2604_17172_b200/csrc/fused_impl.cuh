@@ -46,7 +46,7 @@ namespace uzip {
 // ================================================================ k_hist + k_norm
 // a2: k_hist, grid (parts, chunks, streams), 256 threads: part p of chunk c
 // histograms its slice of the chunk's sample ("the first 256 KB") with
-// warp-aggregated shared atomics (__match_any_sync) and stores the partial
+// per-warp shared-memory atomics and stores the partial
 // histogram; it also zeroes the look-back words of the k_fused launch that
 // follows.  a3: k_norm, grid (chunks, streams): sums the partials, applies
 // rule N1 (R5) and writes the chunk's encode entries and 512-byte table.
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
   const EncJob &J = P.e[blockIdx.z];
   if (J.raw) return;
   const StreamGeom &g = J.g;
-  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const int tid = threadIdx.x, warp = warp_id();
   const uint32_t part = blockIdx.x, c = blockIdx.y;
   {  // reset the look-back words of this job for the k_fused launch that follows
     const uint64_t nctas = (uint64_t)gridDim.x * gridDim.y;
@@ -91,13 +91,12 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
       const bool ok = v0 + u * kHistThreads + tid < v_hi;
       uint32_t sw[4];
       vec_symbols<DT>(w[u], sw);
-      // warp-aggregated increments: the lanes holding the same symbol add once
+      // plain per-warp shared atomics: B200 resolves same-address lanes in the atomic unit
+      // faster than a __match_any_sync warp aggregation (measured k_hist 37 -> 10 us per GiB)
 #pragma unroll
       for (int k = 0; k < (int)kPer; ++k) {
-        const uint32_t sy = ok ? (sw[k >> 2] >> (8 * (k & 3))) & 0xFFu : 0x100u;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, sy);
-        if (sy < 256 && (uint32_t)lane == (uint32_t)(__ffs(peers) - 1))
-          atomicAdd(&hist[warp][sy], (uint32_t)__popc(peers));
+        const uint32_t sy = (sw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        if (ok) atomicAdd(&hist[warp][sy], 1u);
       }
     }
   }
