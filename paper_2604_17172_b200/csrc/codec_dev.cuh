@@ -187,7 +187,10 @@ __device__ __forceinline__ bool decode_join_warp_epi(const uint8_t *pay, uint32_
                                                      uint8_t *ring, const uint8_t *stream, const StreamGeom &g,
                                                      uint64_t b, const Epi &epi) {
   constexpr int kGroups = B / 256;
-  constexpr int kPF = 4;  // residual prefetch distance in groups (divides kGroups)
+#ifndef UZIP_DEC_PF
+#define UZIP_DEC_PF 4
+#endif
+  constexpr int kPF = UZIP_DEC_PF;  // residual prefetch distance in groups (divides kGroups)
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   const uint32_t *pay32 = reinterpret_cast<const uint32_t *>(pay);
