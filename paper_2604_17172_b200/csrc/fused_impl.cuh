@@ -350,7 +350,10 @@ template <int DT, int B>
 struct FusedCfg {
   static constexpr int kVec = VecTraits<DT>::kSym;          // symbols per 16-byte load
   static constexpr int kIters = B / (32 * kVec);            // loads per lane per block
-  static constexpr int kBatch = kIters < 8 ? kIters : 8;
+#ifndef UZIP_SPLIT_BATCH
+#define UZIP_SPLIT_BATCH 8
+#endif
+  static constexpr int kBatch = kIters < UZIP_SPLIT_BATCH ? kIters : UZIP_SPLIT_BATCH;  // 16-byte loads in flight per lane
   static constexpr int kRounds = B / 32;
   static constexpr int kEncTab = 4096;                      // 256 x uint4
   static constexpr int kWarpBuf = B + 256;                  // per warp: symbols/words (E) or payload + ring (D)

@@ -3,8 +3,8 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python -c "from paper_2604_17172_b200 import _build; _build.build()" > /dev/null 2>&1
-SEL_CODEC='tests/test_gpu_codec.py::test_stream_bytes_equal_oracle'
-K_CODEC='W and 163845'
+SEL_CODEC='tests/test_gpu_codec.py::test_stream_bytes_equal_oracle tests/test_gpu_codec.py::test_large_coded_blocks_decoded_in_place tests/test_gpu_codec.py::test_corrupt_and_mismatch'
+K_CODEC='(W and 163845) or in_place or corrupt'
 SEL_COMM='tests/test_gpu_comm.py::test_p2p_bit_exact tests/test_gpu_comm.py::test_allreduce'
 K_COMM='(12305 and 0) or (W-0-2)'
 for tool in memcheck racecheck synccheck; do
