@@ -15,5 +15,5 @@ for tool in memcheck racecheck synccheck; do
     python -m pytest $SEL_COMM -k "$K_COMM" -q -p no:cacheprovider > gpurun_out/sanitize_${tool}_comm.log 2>&1
   echo "$tool comm rc=$?" >> gpurun_out/sanitize_summary.txt
 done
-for f in gpurun_out/sanitize_*.log; do echo "== $f"; grep -E "ERROR SUMMARY|passed|failed|Error" $f | tail -4; done >> gpurun_out/sanitize_summary.txt
+for f in gpurun_out/sanitize_*.log; do echo "== $f"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|passed|failed|Error" $f | tail -4; done >> gpurun_out/sanitize_summary.txt
 cat gpurun_out/sanitize_summary.txt
