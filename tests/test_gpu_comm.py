@@ -522,3 +522,67 @@ def test_collectives_with_codec_params(uz, orc, codec):
             assert np.array_equal(host(outs[r], BF16), refar)
     finally:
         g.close()
+
+
+def _act(n, seed, dtype):
+    """Activation-like values (N(0,1) x per-channel exp(N(0, 0.5^2)) scale, two outlier
+    channels x 64), generated on the GPU so the full BASELINE sizes stay fast."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    h = 4096
+    scale = torch.exp(torch.randn(h, device="cuda", generator=g) * 0.5)
+    scale[7] *= 64
+    scale[1337] *= 64
+    return (torch.randn(n // h, h, device="cuda", generator=g) * scale).reshape(-1).to(TD[dtype])
+
+
+@pytest.mark.parametrize("dtype", [BF16])
+def test_full_size_allreduce_reduce_scatter_n8_sampled(uz, orc, dtype):
+    """BASELINE configs[3] at its largest point: 8 ranks (loopback on one GPU), 256 MiB bf16 activation
+    allreduce and reduce-scatter.  Every rank's allreduce output is bitwise identical, and 8192 sampled
+    elements equal the oracle's fixed-order fp32 fold of the 8 inputs (R11); reduce-scatter shards are
+    checked the same way."""
+    nr, n = 8, (256 << 20) // 2
+    g = Group(uz, nr, max_ctas=148 * 3 // nr, poll_timeout_ms=20000)
+    try:
+        xs = [_act(n, 4000 + r, dtype) for r in range(nr)]
+        outs = [torch.empty_like(x) for x in xs]
+        g.run(lambda r, c, s: c.all_reduce(outs[r], xs[r], s))
+        for r in range(1, nr):
+            assert torch.equal(outs[r].view(VIEW[dtype]), outs[0].view(VIEW[dtype]))
+        idx = np.sort(np.random.default_rng(5).choice(n, 8192, replace=False))
+        it = torch.from_numpy(idx).cuda()
+        ins = [host(x[it], dtype) for x in xs]
+        assert np.array_equal(host(outs[0][it], dtype), orc.reduce(dtype, ins))
+        m = n // nr
+        shards = [torch.empty(m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.reduce_scatter(shards[r], xs[r], s))
+        for r in range(nr):
+            j = np.sort(np.random.default_rng(10 + r).choice(m, 1024, replace=False))
+            jt = torch.from_numpy(j + r * m).cuda()
+            ref = orc.reduce(dtype, [host(x[jt], dtype) for x in xs])
+            assert np.array_equal(host(shards[r][torch.from_numpy(j).cuda()], dtype), ref)
+    finally:
+        g.close()
+
+
+def test_full_size_allgather_4gib_n8(uz):
+    """BASELINE configs[4] at its largest point: 4 GiB allgather output over 8 ranks (512 MiB bf16
+    weights per rank), every rank's output == the concatenation of the inputs, compared in full."""
+    nr, n = 8, (512 << 20) // 2
+    g = Group(uz, nr, max_ctas=148 * 3 // nr, poll_timeout_ms=20000)
+    try:
+        xs = []
+        for r in range(nr):
+            gg = torch.Generator(device="cuda")
+            gg.manual_seed(5000 + r)
+            xs.append((torch.randn(n, device="cuda", generator=gg) * 0.02).to(torch.bfloat16))
+        cat = torch.cat(xs).view(torch.int16)
+        outs = [torch.empty(nr * n, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_gather(outs[r], xs[r], s))
+        for r in range(nr):
+            assert torch.equal(outs[r].view(torch.int16), cat)
+        del outs, cat
+    finally:
+        g.close()
+        torch.cuda.empty_cache()
