@@ -586,3 +586,39 @@ def test_full_size_allgather_4gib_n8(uz):
     finally:
         g.close()
         torch.cuda.empty_cache()
+
+
+def qwen25_7b_shapes():
+    """Qwen2.5-7B-shaped weight tensors: 28 layers x {q [3584,3584] + bias, k/v
+    [512,3584] + bias, o [3584,3584], gate/up [18944,3584], down [3584,18944], 2 norms [3584]} +
+    embed and lm_head [152064,3584] + final norm = 339 tensors, 7,615,616,512 elements."""
+    h, kv, ff, vocab = 3584, 512, 18944, 152064
+    layer = [(h, h), (h,), (kv, h), (kv,), (kv, h), (kv,), (h, h), (ff, h), (ff, h), (h, ff), (h,), (h,)]
+    return [(vocab, h)] + layer * 28 + [(h,), (vocab, h)]
+
+
+def test_full_size_rl_weight_sync_n8(uz):
+    """BASELINE configs[2] in full: every tensor of a Qwen2.5-7B-shaped bf16 model (~15.2 GB, W recipe,
+    own seed per tensor) broadcast from rank 0 to ranks 1-7 (loopback on one GPU), one call per
+    tensor (the sub-1 MiB biases and norms take the raw path); every receiver's bytes == the root's."""
+    shapes = qwen25_7b_shapes()
+    assert len(shapes) == 339 and sum(int(np.prod(s)) for s in shapes) == 7_615_616_512
+    nr = 8
+    g = Group(uz, nr, max_ctas=148 * 3 // nr, poll_timeout_ms=20000)
+    try:
+        big = max(int(np.prod(s)) for s in shapes)
+        bufs = [torch.empty(big, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+        gg = torch.Generator(device="cuda")
+        for i, s in enumerate(shapes):
+            n = int(np.prod(s))
+            gg.manual_seed(7000 + i)
+            bufs[0][:n].copy_(torch.randn(n, device="cuda", generator=gg) * 0.02)
+            for r in range(1, nr):
+                bufs[r][:n].fill_(7)
+            g.run(lambda r, c, st: c.broadcast(bufs[r][:n], 0, st))
+            ref = bufs[0][:n].view(torch.int16)
+            for r in range(1, nr):
+                assert torch.equal(bufs[r][:n].view(torch.int16), ref), (i, s, r)
+    finally:
+        g.close()
+        torch.cuda.empty_cache()
