@@ -622,3 +622,38 @@ def test_full_size_rl_weight_sync_n8(uz):
     finally:
         g.close()
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("mode", ["one_message", "per_layer"])
+def test_full_size_kv_cache_p2p(uz, mode):
+    """BASELINE configs[4] KV-cache transfer in full: Llama-3-8B vLLM KV blocks for 7680 tokens
+    (480 blocks x 32 layers x 64 KiB = 960 MiB bf16; K = N(0,1) x per-dim exp(N(0, 0.5^2)), V = N(0,1)),
+    sent GPU "0" -> "1" (loopback) as one message or as 32 per-layer messages of 30 MiB; recv == send."""
+    g = Group(uz, 2, max_ctas=296, poll_timeout_ms=20000)
+    try:
+        gg = torch.Generator(device="cuda")
+        gg.manual_seed(8000)
+        layers, nb = 32, 480
+        kscale = torch.exp(torch.randn(layers, 1, 1, 8, 128, device="cuda", generator=gg) * 0.5)
+        k = torch.randn(layers, nb, 16, 8, 128, device="cuda", generator=gg) * kscale
+        v = torch.randn(layers, nb, 16, 8, 128, device="cuda", generator=gg)
+        x = torch.stack([k, v], dim=2).to(torch.bfloat16).contiguous()  # [layer, block, K/V, 16, 8, 128]
+        del k, v
+        assert x.numel() * 2 == 960 << 20
+        y = torch.zeros_like(x)
+        if mode == "one_message":
+            g.run(lambda r, c, s: c.send(x.view(-1), 1, s) if r == 0 else c.recv(y.view(-1), 0, s))
+        else:
+            def per_layer(r, c, s):
+                for l in range(layers):
+                    if r == 0:
+                        c.send(x[l].view(-1), 1, s)
+                    else:
+                        c.recv(y[l].view(-1), 0, s)
+            g.run(per_layer)
+        assert torch.equal(y.view(torch.int16), x.view(torch.int16))
+        st = g.comms[0].stats()
+        assert 0.5 < st["wire_bytes"] / st["raw_bytes"] < 0.85, st  # compressed (activation-like ratio)
+    finally:
+        g.close()
+        torch.cuda.empty_cache()
