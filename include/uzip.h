@@ -143,7 +143,11 @@ UZIP_API uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, i
                              uzip_allgather_fn bootstrap, void *ctx, const uzip_config_t *cfg);
 
 /* Single-process init of `nranks` communicators (like ncclCommInitAll);
- * devices[r] may repeat (loopback: several ranks on one GPU). */
+ * devices[r] may repeat (loopback: several ranks on one GPU).  Ranks that
+ * share a GPU (here, or IPC ranks whose GPU UUIDs match) run their persistent
+ * kernels side by side: a launch whose decode items spin on a peer holds at
+ * most 1/k of the CTA slots for k co-resident ranks, and slot credits are
+ * always awaited by a one-thread kernel, so every producer finds an SM. */
 UZIP_API uzip_status_t uzip_comm_init_all(uzip_comm_t *comms, int nranks, const int *devices,
                                  const uzip_config_t *cfg);
 UZIP_API uzip_status_t uzip_comm_destroy(uzip_comm_t comm);
@@ -151,7 +155,10 @@ UZIP_API uzip_status_t uzip_comm_destroy(uzip_comm_t comm);
 /* Split-send P2P: the residual plane leaves for the peer as soon
  * as it is split, the entropy-coded exponents follow; the receiver decodes as
  * blocks land.  A send on rank a matches the next recv on `peer` with the
- * same count and dtype (FIFO per ordered pair, like NCCL). */
+ * same count and dtype (FIFO per ordered pair, like NCCL).  As with NCCL,
+ * calls of one communicator are issued in one order on one stream; a send and
+ * a recv of the same rank placed on two streams to run concurrently may wait
+ * on each other for SMs (the kernels are persistent and spin on their peer). */
 UZIP_API uzip_status_t uzip_send(const void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t comm,
                         void *stream);
 UZIP_API uzip_status_t uzip_recv(void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t comm,
