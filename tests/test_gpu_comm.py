@@ -657,3 +657,56 @@ def test_full_size_kv_cache_p2p(uz, mode):
     finally:
         g.close()
         torch.cuda.empty_cache()
+
+
+def test_back_to_back_collectives_rank_major_issue(uz, orc):
+    """A queue of collectives issued without synchronisation, rank by rank (rank 0 enqueues its whole
+    sequence before rank 1 enqueues anything): allreduce / allgather / reduce-scatter of 2-32 MiB,
+    several rounds through 8 MiB slots, so producers of later calls owe credits to consumers that are
+    still queued.  Allgather compared in full; allreduce / reduce-scatter on sampled elements vs the
+    oracle's fixed-order fold."""
+    nr = 4
+    g = Group(uz, nr, staging_bytes=16 << 20, max_ctas=148 * 3 // nr, poll_timeout_ms=20000)
+    try:
+        ops = [("ar", 15 << 20), ("ag", 4 << 20), ("rs", 12 << 20), ("ar", 1 << 20), ("ag", 8 << 20),
+               ("ar", 8 << 20), ("rs", 2 << 20), ("ar", 16 << 20)]  # element counts (bf16)
+        data, outs = [], []
+        for k, (op, n) in enumerate(ops):
+            xs = [_act(n, 9000 + 10 * k + r, BF16) for r in range(nr)]
+            data.append(xs)
+            m = {"ar": n, "ag": n * nr, "rs": n // nr}[op]
+            outs.append([torch.empty(m, dtype=torch.bfloat16, device="cuda") for _ in range(nr)])
+        torch.cuda.synchronize()
+        for r, c in enumerate(g.comms):  # rank-major issue, no synchronisation in between
+            s = g.streams[r]
+            with torch.cuda.stream(s):
+                for k, (op, n) in enumerate(ops):
+                    if op == "ar":
+                        c.all_reduce(outs[k][r], data[k][r], s)
+                    elif op == "ag":
+                        c.all_gather(outs[k][r], data[k][r], s)
+                    else:
+                        c.reduce_scatter(outs[k][r], data[k][r], s)
+        torch.cuda.synchronize()
+        assert [c.async_error() for c in g.comms] == [0] * nr
+        rng = np.random.default_rng(17)
+        for k, (op, n) in enumerate(ops):
+            xs, ys = data[k], outs[k]
+            if op == "ag":
+                cat = torch.cat(xs).view(torch.int16)
+                for r in range(nr):
+                    assert torch.equal(ys[r].view(torch.int16), cat), (k, r)
+            elif op == "ar":
+                for r in range(1, nr):
+                    assert torch.equal(ys[r].view(torch.int16), ys[0].view(torch.int16)), (k, r)
+                it = torch.from_numpy(np.sort(rng.choice(n, 2048, replace=False))).cuda()
+                ref = orc.reduce(BF16, [host(x[it], BF16) for x in xs])
+                assert np.array_equal(host(ys[0][it], BF16), ref), k
+            else:
+                m = n // nr
+                for r in range(nr):
+                    j = np.sort(rng.choice(m, 512, replace=False))
+                    ref = orc.reduce(BF16, [host(x[torch.from_numpy(j + r * m).cuda()], BF16) for x in xs])
+                    assert np.array_equal(host(ys[r][torch.from_numpy(j).cuda()], BF16), ref), (k, r)
+    finally:
+        g.close()
