@@ -152,6 +152,7 @@ def run(args):
             return round(raw / (t / 1e3) / GB, 3)
 
         ablation["chunked_8MiB_GBps"] = p2p_with(pipe_chunk_bytes=8 << 20)
+        ablation["block_sweep_GBps"] = {str(bs): p2p_with(block_symbols=bs) for bs in (1024, 2048)}  # 4096: value
         ablation["sm_limited_GBps"] = {str(m): p2p_with(max_ctas=m) for m in (16, 37, 74, 148)}
 
     # e2e through the public API with host buffers: the sender copies its input from pinned host memory

@@ -9,7 +9,9 @@ bytes:
                     256 MiB round, tile-granular overlap);
   * chunked_8MiB    the same calls with pipe_chunk_bytes = 8 MiB: one UZB1 stream and one launch per 8 MiB
                     chunk -- the paper's "8 MB chunked pipeline" (P:540) / NCCL-slice granularity (P:815);
-  * chunked_1MiB    the same at 1 MiB;
+  * chunked_1MiB    the same at 1 MiB (chunked_64MiB / chunked_256MiB: the rest of BASELINE configs[1]'s
+                    pipeline-chunk sweep);
+  * block_1024/2048 the fused path with 1024- / 2048-symbol codec blocks (configs[1]'s block-size sweep);
   * encode_send     uzip_compress of the whole message, a device copy of the stream (the wire), then
                     uzip_decompress -- serial, no overlap (fig:compare_with_native_pipeline);
   * sm_limited      the fused path with each side's kernel capped at max_ctas CTAs (fig:resource_usage;
@@ -95,6 +97,10 @@ def main():
     p2p_leg("fused", max_ctas=2 * 148)
     p2p_leg("chunked_8MiB", max_ctas=2 * 148, pipe_chunk_bytes=8 << 20)
     p2p_leg("chunked_1MiB", max_ctas=2 * 148, pipe_chunk_bytes=1 << 20)
+    for mib in (64, 256):  # BASELINE configs[1] pipeline-chunk sweep (whole slots = "fused" above)
+        p2p_leg(f"chunked_{mib}MiB", max_ctas=2 * 148, pipe_chunk_bytes=mib << 20)
+    for bs in (1024, 2048):  # ... and its codec block-size sweep (4096 = "fused")
+        p2p_leg(f"block_{bs}", max_ctas=2 * 148, block_symbols=bs)
     for m in (16, 37, 74, 148):
         p2p_leg(f"sm_limited_{m}ctas", max_ctas=m)
 
