@@ -183,7 +183,10 @@ void base_plan(uzip_comm *c, Plan &p, int dt) {
   p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
   static const uint32_t stress = (uint32_t)strtoul(getenv("UZIP_STRESS") ? getenv("UZIP_STRESS") : "0", nullptr, 0);
   p.stress = stress;
-  p.share = c->share ? c->share : 1;
+  // debug knob: UZIP_SHARE_CAP=0 sizes launches as if the GPU were not shared (measurement of one
+  // side alone only -- co-resident ranks that run concurrently need the cap)
+  static const bool share_cap = !(getenv("UZIP_SHARE_CAP") && atoi(getenv("UZIP_SHARE_CAP")) == 0);
+  p.share = (c->share && share_cap) ? c->share : 1;
 }
 
 // Encode job of `n` elements at `in` (round stream) into destinations dsts.
@@ -245,6 +248,15 @@ void dec_job(uzip_comm *c, Plan &p, int j, int dt, uint64_t n, bool compressed, 
   }
   J.out = out;
   J.done = ws_done(c, j);
+  // Plain decode jobs take their tiles in runs: a CTA's consecutive tickets are ~grid tiles apart,
+  // i.e. in another 8 MiB chunk, so per-tile items rebuilt the 4096-slot decode table for every
+  // tile.  Runs stay short next to the message so the receiver still follows the sender closely.
+#ifndef UZIP_DEC_RUN_MAX
+#define UZIP_DEC_RUN_MAX 8
+#endif
+  J.run = 1;
+  if (compressed && J.nsrc == 1 && me_idx < 0)
+    J.run = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(UZIP_DEC_RUN_MAX, J.ntiles / 1024));
   p.nd_jobs = j + 1;
 }
 
@@ -296,7 +308,7 @@ uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
     }
   }
   for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
-  for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += p.d[j].ntiles;
+  for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += items_of(p.d[j]);
   p.n_c_items = p.has_copy ? p.c.ntiles : 0;
   if (compressed && p.ne > 0) {
     if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;

@@ -1258,12 +1258,14 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
     } else {
       uint64_t k = it - ne - nc;  // job-major over the decode jobs
       int j = 0;
-      while (j + 1 < P.nd_jobs && k >= P.d[j].ntiles) k -= P.d[j++].ntiles;
-      if constexpr (RED) {
-        if (P.d[j].nsrc > 1) red_item<DT, B>(P, P.d[j], j, k, smem, S, dec_key);
-        else dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
-      } else {
-        dec_item<DT, B, RED>(P, P.d[j], j, k, smem, S, dec_key, fwd_done);
+      while (j + 1 < P.nd_jobs && k >= items_of(P.d[j])) k -= items_of(P.d[j++]);
+      const DecJob &Jd = P.d[j];
+      if (RED && Jd.nsrc > 1) {
+        red_item<DT, B>(P, Jd, j, k, smem, S, dec_key);
+      } else {  // a run of consecutive tiles (one decode-table build for the run)
+        const uint64_t r = Jd.run > 1 ? Jd.run : 1, t1 = min(Jd.ntiles, (k + 1) * r);
+        for (uint64_t t = k * r; t < t1; ++t)  // after an abort every later tile returns at once
+          dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);
       }
     }
     __syncthreads();

@@ -63,6 +63,8 @@ struct DecJob {
   uint32_t epoch[kMaxRanks];
   uint8_t *out;                             // output of this stream / shard
   uint32_t *done;                           // tiles finished (self-resetting counter in ws)
+  uint32_t run;                             // consecutive tiles per D item (>= 1): one decode-table
+                                            // build serves the run instead of one build per tile
   // relay (broadcast): every received tile is forwarded, as received, to nfwd peers before it is
   // decoded; the compressed bytes travel on without re-encoding (weight-sync broadcast)
   uint32_t nfwd;
@@ -71,6 +73,11 @@ struct DecJob {
   const unsigned long long *fcredit[kMaxRanks];  // local credit words for those slots
   uint32_t fepoch[kMaxRanks];
 };
+
+// D items of a decode job (runs of `run` consecutive tiles).
+__host__ __device__ inline uint64_t items_of(const DecJob &J) {
+  return J.run > 1 ? (J.ntiles + J.run - 1) / J.run : J.ntiles;
+}
 
 struct CopyJob {
   const uint8_t *src;

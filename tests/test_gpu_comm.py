@@ -710,3 +710,23 @@ def test_back_to_back_collectives_rank_major_issue(uz, orc):
                     assert np.array_equal(host(ys[r][torch.from_numpy(j).cuda()], BF16), ref), (k, r)
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("chunk_blocks", [0, 8])
+def test_p2p_decode_runs(uz, chunk_blocks):
+    """A ~1 GiB message in one round (16384+ tiles): the receiver takes its tiles in runs of 8 (one
+    decode-table build per run); with 8-block chunks every tile of a run has its own table, and the
+    last run is ragged.  recv == send, both sides' kernels sized for the whole GPU in turn."""
+    g = Group(uz, 2, staging_bytes=3 << 30, max_ctas=296, poll_timeout_ms=20000,
+              **({"chunk_blocks": chunk_blocks} if chunk_blocks else {}))
+    try:
+        n = (1 << 29) + 3 * 4096 * 8 + 4096 + 5  # ragged: a partial last tile and a raw tail
+        gg = torch.Generator(device="cuda")
+        gg.manual_seed(77)
+        x = (torch.randn(n, device="cuda", generator=gg) * 0.02).to(torch.bfloat16)
+        y = torch.zeros_like(x)
+        g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else c.recv(y, 0, s))
+        assert torch.equal(y.view(torch.int16), x.view(torch.int16))
+    finally:
+        g.close()
+        torch.cuda.empty_cache()
