@@ -277,6 +277,13 @@ void fwd_setup(uzip_comm *c, Plan &p, int j, const std::vector<int> &dsts) {
 }
 
 uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
+  for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
+  for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += items_of(p.d[j]);
+  p.n_c_items = p.has_copy ? p.c.ntiles : 0;
+  // the sampled tables need no slot: they are built before the credit wait, which they then overlap
+  if (compressed && p.ne > 0) {
+    if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;
+  }
   // From the third launch of a call on, a slot's credit comes from a consumer
   // launch of this same call: wait for it in k_credit (one thread) instead of
   // in every CTA of the fused kernel, which would hold SM slots the consumer
@@ -284,8 +291,11 @@ uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
   // wait this way: a credit owed by an earlier call is just as likely to come
   // from a consumer kernel that is still queued behind the spinning producer
   // (measured: 8 back-to-back 30 MiB sends issued before their recvs timed out).
+#ifndef UZIP_SHARED_CREDIT_KERNEL
+#define UZIP_SHARED_CREDIT_KERNEL 1
+#endif
   const bool first_rounds = c->call_rounds++ < 2;
-  if (!first_rounds || c->share > 1) {
+  if (!first_rounds || (UZIP_SHARED_CREDIT_KERNEL && c->share > 1)) {
     CreditWait w;
     memset(&w, 0, sizeof w);
     for (int j = 0; j < p.ne; ++j)
@@ -306,12 +316,6 @@ uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
       if (launch_credit_wait(w, st) != cudaSuccess) return UZIP_ERR_CUDA;
       p.credit_ready = 1;
     }
-  }
-  for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
-  for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += items_of(p.d[j]);
-  p.n_c_items = p.has_copy ? p.c.ntiles : 0;
-  if (compressed && p.ne > 0) {
-    if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;
   }
   if (launch_fused(p.dtype, p, st, (int)c->cfg.max_ctas) != cudaSuccess) return UZIP_ERR_CUDA;
   return UZIP_OK;
