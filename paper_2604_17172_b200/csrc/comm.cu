@@ -254,8 +254,11 @@ void dec_job(uzip_comm *c, Plan &p, int j, int dt, uint64_t n, bool compressed, 
 #ifndef UZIP_DEC_RUN_MAX
 #define UZIP_DEC_RUN_MAX 8
 #endif
+  // Reduce jobs with one remote source (2 ranks) reuse that source's table across the run too; with
+  // more sources the table changes with every source of a tile anyway, so they keep single tiles.
   J.run = 1;
-  if (compressed && J.nsrc == 1 && me_idx < 0)
+  const int remote = (int)J.nsrc - (me_idx >= 0 ? 1 : 0);
+  if (compressed && remote == 1)
     J.run = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(UZIP_DEC_RUN_MAX, J.ntiles / 1024));
   p.nd_jobs = j + 1;
 }

@@ -1260,12 +1260,16 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
       int j = 0;
       while (j + 1 < P.nd_jobs && k >= items_of(P.d[j])) k -= items_of(P.d[j++]);
       const DecJob &Jd = P.d[j];
-      if (RED && Jd.nsrc > 1) {
-        red_item<DT, B>(P, Jd, j, k, smem, S, dec_key);
-      } else {  // a run of consecutive tiles (one decode-table build for the run)
-        const uint64_t r = Jd.run > 1 ? Jd.run : 1, t1 = min(Jd.ntiles, (k + 1) * r);
-        for (uint64_t t = k * r; t < t1; ++t)  // after an abort every later tile returns at once
+      // a run of consecutive tiles (one decode-table build per source for the run); after an abort
+      // every later tile of the run returns at once
+      const uint64_t r = Jd.run > 1 ? Jd.run : 1, t1 = min(Jd.ntiles, (k + 1) * r);
+      for (uint64_t t = k * r; t < t1; ++t) {
+        if constexpr (RED) {
+          if (Jd.nsrc > 1) red_item<DT, B>(P, Jd, j, t, smem, S, dec_key);
+          else dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);
+        } else {
           dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);
+        }
       }
     }
     __syncthreads();
