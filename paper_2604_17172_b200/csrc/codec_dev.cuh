@@ -21,48 +21,63 @@ __device__ __forceinline__ uint32_t block_size(uint32_t d, uint32_t B, bool &bad
 
 // Decode table of one chunk: f:12 <<20 | (slot-cdf):12 <<8 | sym:8 (a7).
 // All 256 threads; returns false (uniformly) if the table is invalid.  Every
-// thread fills its own 16 slots: mark each symbol's first slot, running max
-// over the thread's slots, block-wide exclusive max-scan -- balanced over the
-// warps (filling symbol by symbol left the warp owning the dominant exponents
-// with ~128 serial store iterations while the others waited at the barrier).
-// `scr`: 2 KiB of smem scratch (per-symbol f and cdf).
+// warp reads the 256 frequencies itself (8 per lane, one 16-byte load) and
+// scans them, so the cdf needs no block-wide exchange; warp w owns slots
+// [512w, 512w+512): it zeroes them, marks the first slot of each symbol that
+// starts there, and each lane fills its 16 slots by a running max over the
+// marks (balanced -- filling symbol by symbol left the warp owning the
+// dominant exponents with ~128 serial stores).  One block barrier (for the
+// per-symbol f/cdf scratch) instead of six; the caller's barrier publishes
+// the table.  `scr`: 2 KiB of smem scratch (per-symbol f and cdf).
 __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, uint32_t *s_red, uint32_t *scr) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  const uint32_t f = ld_cg_u16(ft + tid);
-  uint32_t incl = f;
+  (void)s_red;
+  const int lane = threadIdx.x & 31, warp = warp_id();
+  const uint4 q = ld_cg_v4(ft + 8 * lane);
+  const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+  uint32_t f[8], c[8], loc = 0, zero = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    f[k] = (w4[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+    c[k] = loc;
+    loc += f[k];
+    zero |= f[k] == 0;
+  }
+  uint32_t incl = loc;
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    const uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, incl, o);
     if (lane >= o) incl += tt;
   }
-  const uint32_t anyzero = __ballot_sync(0xFFFFFFFFu, f == 0);
-  if (lane == 31) s_red[warp] = incl | (anyzero ? 0x80000000u : 0u);
-  __syncthreads();
-  uint32_t woff = 0, fsum = 0, bad = 0;
-  for (int w = 0; w < kWarps; ++w) {
-    const uint32_t v = s_red[w];
-    bad |= v >> 31;
-    if (w < warp) woff += v & 0x7FFFFFFFu;
-    fsum += v & 0x7FFFFFFFu;
+  const uint32_t fsum = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  if (fsum != kM || __any_sync(0xFFFFFFFFu, zero)) return false;  // same table in every warp: uniform
+  const uint32_t base = incl - loc;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] += base;
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      scr[8 * lane + k] = f[k];
+      scr[256 + 8 * lane + k] = c[k];
+    }
   }
-  __syncthreads();
-  if (fsum != kM || bad) return false;
-  const uint32_t cdf = woff + incl - f;
-  scr[tid] = f;
-  scr[256 + tid] = cdf;
-  uint4 *d4 = reinterpret_cast<uint4 *>(dtab) + 4 * tid;
+  const uint32_t w0 = 512u * (uint32_t)warp;  // this warp's slots [w0, w0 + 512)
+  uint4 *d4 = reinterpret_cast<uint4 *>(dtab + w0 + 16 * lane);
 #pragma unroll
   for (int i = 0; i < 4; ++i) d4[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  dtab[cdf] = (uint32_t)tid;  // distinct first slots (every f >= 1)
-  __syncthreads();
+  __syncwarp();
+  // marks; and the symbol covering slot w0 (the last one starting at or before it)
+  uint32_t cover = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if ((c[k] >> 9) == (uint32_t)warp) dtab[c[k]] = 8u * lane + k;  // distinct first slots (f >= 1)
+    if (c[k] <= w0) cover = 8u * lane + k;
+  }
+  for (int o = 16; o; o >>= 1) cover = max(cover, __shfl_xor_sync(0xFFFFFFFFu, cover, o));
+  __syncwarp();
   uint32_t v[16];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint4 q = d4[i];
-    v[4 * i] = q.x;
-    v[4 * i + 1] = q.y;
-    v[4 * i + 2] = q.z;
-    v[4 * i + 3] = q.w;
+    const uint4 t = d4[i];
+    v[4 * i] = t.x, v[4 * i + 1] = t.y, v[4 * i + 2] = t.z, v[4 * i + 3] = t.w;
   }
   uint32_t m = 0;
 #pragma unroll
@@ -72,24 +87,21 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
     const uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, inc, o);
     if (lane >= o) inc = max(inc, tt);
   }
-  if (lane == 31) s_red[warp] = inc;
-  __syncthreads();
   uint32_t pre = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
-  if (lane == 0) pre = 0;
-  for (int w = 0; w < warp; ++w) pre = max(pre, s_red[w]);
+  pre = max(lane == 0 ? 0u : pre, cover);
+  __syncthreads();  // scr (warp 0) visible
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     uint32_t e[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t sym = max(pre, v[4 * i + k]);
-      const uint32_t slot = 16u * tid + 4 * i + k;
+      const uint32_t slot = w0 + 16u * lane + 4 * i + k;
       e[k] = (scr[sym] << 20) | ((slot - scr[256 + sym]) << 8) | sym;
     }
     d4[i] = make_uint4(e[0], e[1], e[2], e[3]);
   }
-  __syncthreads();  // s_red and scr are free again
-  return true;
+  return true;  // the caller's barrier publishes dtab (and frees scr)
 }
 
 // a8: one warp decodes the K-word block in `pay` (smem) into 8-bit symbols.
