@@ -145,34 +145,12 @@ __global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__
       const uint64_t chunk_stop = min(cb1, c_end);
       __syncthreads();
       if (tid == 0) s_bad = 0;
-      // ---- a7: decode table of chunk c: f:12 <<20 | (slot-cdf):12 <<8 | sym:8
-      const uint16_t *ft = reinterpret_cast<const uint16_t *>(in + g.off_tab + 512 * c);
-      const uint32_t f = ft[tid];
-      uint32_t incl = f;
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t tt = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += tt;
-      }
-      if (lane == 31) s_red[warp] = incl;
-      __syncthreads();
-      uint32_t woff = 0, fsum = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        if (w < warp) woff += s_red[w];
-        fsum += s_red[w];
-      }
-      const uint32_t cdf = woff + incl - f;
-      if (fsum != kM) {
+      // ---- a7: decode table of chunk c (the shared builder; warp 0's staging buffer is its scratch,
+      // free until the bookkeeping barriers below have published the table)
+      if (!build_dtab(reinterpret_cast<const uint16_t *>(in + g.off_tab + 512 * c), dtab, s_red,
+                      reinterpret_cast<uint32_t *>(smem + DecShared::kTab + DecShared::kOff))) {
         set_err(ws, UZIP_ERR_CORRUPT_STREAM);
-        break;  // uniform: every thread saw the same sum
-      }
-      if (f == 0) s_bad = 1;
-      // thread tid owns symbol tid; the 32 lanes of a warp fill the slots of the
-      // warp's 32 symbols one symbol at a time
-      for (int k = 0; k < 32; ++k) {
-        const uint32_t fk = __shfl_sync(0xFFFFFFFFu, f, k);
-        const uint32_t ck = __shfl_sync(0xFFFFFFFFu, cdf, k);
-        const uint32_t sk = (uint32_t)(warp * 32 + k);
-        for (uint32_t t = lane; t < fk; t += 32) dtab[ck + t] = (fk << 20) | (t << 8) | sk;
+        break;  // uniform: every warp read the same table
       }
       // ---- chunk bookkeeping: bytes before s0 inside the chunk; the CTA that
       // owns the chunk's first block also checks chunk_off[c] + sum == next.
