@@ -54,9 +54,7 @@ __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom 
   if (d == kRawBlock) {
     join_block<DT, B>(src, in, g, b, dst);  // raw symbols joined straight from the stream
   } else if (size <= (uint32_t)DecShared::kStage) {
-    uint4 *dstv = reinterpret_cast<uint4 *>(pay);
-    for (uint32_t i = lane; i < size / 16; i += 32) dstv[i] = ld_cg_v4(src + 16 * i);
-    __syncwarp();
+    stage_block(src, size / 16, pay);
     ok = decode_join_warp<DT, B>(pay, d, dtab, ring, in, g, b, dst);
   } else {
     // rare: a coded block larger than the staging area is decoded in place from global memory

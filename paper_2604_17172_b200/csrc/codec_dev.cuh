@@ -104,6 +104,25 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
   return true;  // the caller's barrier publishes dtab (and frees scr)
 }
 
+// Stage n16 16-byte words of a coded block into the warp's smem buffer with cp.async (L2 -> smem,
+// .cg: never through L1, the bytes may have been written by a peer GPU): every lane's copies are
+// in flight at once and hold no registers (a register-batched copy spilled the decoder).
+#ifndef UZIP_STAGE_ASYNC
+#define UZIP_STAGE_ASYNC 1
+#endif
+__device__ __forceinline__ void stage_block(const uint8_t *src, uint32_t n16, uint8_t *pay) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (UZIP_STAGE_ASYNC) {
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(pay);
+    for (uint32_t i = lane; i < n16; i += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + 16 * i), "l"(src + 16 * i) : "memory");
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+  } else {
+    for (uint32_t i = lane; i < n16; i += 32) reinterpret_cast<uint4 *>(pay)[i] = ld_cg_v4(src + 16 * i);
+  }
+  __syncwarp();
+}
+
 // a8: one warp decodes the K-word block in `pay` (smem) into 8-bit symbols.
 // Returns false if the block is corrupt (word overrun, end state != L).
 template <int B>

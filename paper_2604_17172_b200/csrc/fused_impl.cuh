@@ -40,6 +40,9 @@
 #ifndef UZIP_ENC_MINB
 #define UZIP_ENC_MINB 3   // resident CTAs per SM targeted by launches with encode items (measured)
 #endif
+#ifndef UZIP_DEC_ONLY_MINB
+#define UZIP_DEC_ONLY_MINB 4  // ... and by decode-only launches (P2P / broadcast receivers)
+#endif
 
 namespace uzip {
 
@@ -882,10 +885,7 @@ __device__ __forceinline__ void tile_block(const uint8_t *stream, const StreamGe
 // Stage block payload into smem (warp).
 __device__ __forceinline__ void stage_payload(const uint8_t *stream, const StreamGeom &g, unsigned long long off,
                                               uint32_t size, uint8_t *pay) {
-  const int lane = threadIdx.x & 31;
-  const uint8_t *p = stream + g.off_pay + off;
-  for (uint32_t i = lane; i < size / 16; i += 32) reinterpret_cast<uint4 *>(pay)[i] = ld_cg_v4(p + 16 * i);
-  __syncwarp();
+  stage_block(stream + g.off_pay + off, size / 16, pay);
 }
 
 // Copy stream bytes [o, o+len) from the local staging to the same offset in
@@ -1351,7 +1351,7 @@ cudaError_t launch_fused_t(const Plan &p, cudaStream_t st, int max_ctas) {
     return launch_fused_k<DT, B, RED, UZIP_RED_MINB>(p, st, max_ctas);
   } else {
     if (p.n_e_items > 0) return launch_fused_k<DT, B, RED, UZIP_ENC_MINB>(p, st, max_ctas);
-    return launch_fused_k<DT, B, RED, 4>(p, st, max_ctas);
+    return launch_fused_k<DT, B, RED, UZIP_DEC_ONLY_MINB>(p, st, max_ctas);
   }
 }
 
@@ -1372,9 +1372,9 @@ cudaError_t preload_t() {
     e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_ENC_MINB>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_ENC_MINB>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, UZIP_ENC_MINB>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, 4>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, 4>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_DEC_ONLY_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_DEC_ONLY_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, UZIP_DEC_ONLY_MINB>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_hist<DT>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_norm<DT>);
   }
