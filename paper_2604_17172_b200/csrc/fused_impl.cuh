@@ -1226,7 +1226,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
 // MINB: resident CTAs per SM the register allocation targets.  Launches with
 // encode items use UZIP_ENC_MINB (3: 85 registers, measured fastest for the
 // encoder); decode-only launches use 4 (64 registers, like k_decode).
-template <int DT, int B, bool RED, int MINB>
+template <int DT, int B, bool RED, int MINB, bool DONLY = false>
 __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Plan P) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ FusedShared S;
@@ -1247,21 +1247,12 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
     uint32_t nxt = 0;
     if (tid == 0) S.tk[par ^ 1] = nxt = atomicAdd(P.ticket, 1u);  // next ticket, read after the item's last barrier
     nxt = __shfl_sync(0xFFFFFFFFu, nxt, 0);  // warp 0 knows it now (L2 prefetch of that tile)
-    const bool coded_e = it < ne && !P.e[it % (uint64_t)P.ne].raw;
-    if (pd.job >= 0 && !coded_e) resolve_pending<DT, B>(P, S, ring, pd);
-    if (it < ne) {
-      const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
-      enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, ring, P.ring_bytes, pd,
-                      warp_id() == 0 ? (uint64_t)nxt : ~0ull);
-    } else if (it < ne + nc) {
-      copy_item(P.c, it - ne);
-    } else {
-      uint64_t k = it - ne - nc;  // job-major over the decode jobs
+    // D items: job-major; a run of consecutive tiles per item (one decode-table build per source for
+    // the run); after an abort every later tile of the run returns at once
+    auto decode_items = [&](uint64_t k) {
       int j = 0;
       while (j + 1 < P.nd_jobs && k >= items_of(P.d[j])) k -= items_of(P.d[j++]);
       const DecJob &Jd = P.d[j];
-      // a run of consecutive tiles (one decode-table build per source for the run); after an abort
-      // every later tile of the run returns at once
       const uint64_t r = Jd.run > 1 ? Jd.run : 1, t1 = min(Jd.ntiles, (k + 1) * r);
       for (uint64_t t = k * r; t < t1; ++t) {
         if constexpr (RED) {
@@ -1271,11 +1262,29 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
           dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);
         }
       }
+    };
+    if constexpr (DONLY) {
+      // decode-only launch (P2P / broadcast receivers): no E/C item code in this instantiation, so
+      // its register budget is the decoder's alone
+      decode_items(it);
+    } else {
+      const bool coded_e = it < ne && !P.e[it % (uint64_t)P.ne].raw;
+      if (pd.job >= 0 && !coded_e) resolve_pending<DT, B>(P, S, ring, pd);
+      if (it < ne) {
+        const int j = (int)(it % (uint64_t)P.ne);  // tile-major over the encode streams
+        enc_item<DT, B>(P, P.e[j], j, it / (uint64_t)P.ne, smem, S, enc_key, credit_done, ring, P.ring_bytes, pd,
+                        warp_id() == 0 ? (uint64_t)nxt : ~0ull);
+      } else if (it < ne + nc) {
+        copy_item(P.c, it - ne);
+      } else {
+        decode_items(it - ne - nc);
+      }
     }
     __syncthreads();
     it = uniform_u64(S.tk[par ^ 1]);
   }
-  if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);
+  if constexpr (!DONLY)
+    if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);
   if (tid == 0) {  // the last CTA out resets the ticket for the next launch
     __threadfence();
     if (atomicAdd(P.ticket + 1, 1u) == gridDim.x - 1) {
@@ -1316,14 +1325,14 @@ cudaError_t launch_tables_t(const Plan &p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int DT, int B, bool RED, int MINB>
+template <int DT, int B, bool RED, int MINB, bool DONLY = false>
 cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   using C = FusedCfg<DT, B>;
   const bool dec = p.n_d_items > 0;
   // the ring parks coded tiles (encode launches only; none in the reduce variant)
   p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
   const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0);
-  auto kern = k_fused<DT, B, RED, MINB>;
+  auto kern = k_fused<DT, B, RED, MINB, DONLY>;
   static int attr_set = 0;
   if (attr_set < C::smem(true, RED)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(true, RED));
@@ -1351,6 +1360,7 @@ cudaError_t launch_fused_t(const Plan &p, cudaStream_t st, int max_ctas) {
     return launch_fused_k<DT, B, RED, UZIP_RED_MINB>(p, st, max_ctas);
   } else {
     if (p.n_e_items > 0) return launch_fused_k<DT, B, RED, UZIP_ENC_MINB>(p, st, max_ctas);
+    if (p.n_c_items == 0) return launch_fused_k<DT, B, RED, UZIP_DEC_ONLY_MINB, true>(p, st, max_ctas);
     return launch_fused_k<DT, B, RED, UZIP_DEC_ONLY_MINB>(p, st, max_ctas);
   }
 }
@@ -1375,6 +1385,9 @@ cudaError_t preload_t() {
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_DEC_ONLY_MINB>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_DEC_ONLY_MINB>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, UZIP_DEC_ONLY_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_DEC_ONLY_MINB, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_DEC_ONLY_MINB, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, UZIP_DEC_ONLY_MINB, true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_hist<DT>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_norm<DT>);
   }

@@ -16,9 +16,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2604_17172_b200", "libuzip.so")
 KERNELS = {
-    "k_fused_bf16_b4096_encode": "_ZN4uzip7k_fusedILi0ELi4096ELb0ELi3EEEvNS_4PlanE",
-    "k_fused_bf16_b4096_decode": "_ZN4uzip7k_fusedILi0ELi4096ELb0ELi4EEEvNS_4PlanE",
-    "k_fused_bf16_b4096_reduce": "_ZN4uzip7k_fusedILi0ELi4096ELb1ELi3EEEvNS_4PlanE",
+    "k_fused_bf16_b4096_encode": "_ZN4uzip7k_fusedILi0ELi4096ELb0ELi3ELb0EEEvNS_4PlanE",
+    "k_fused_bf16_b4096_decode": "_ZN4uzip7k_fusedILi0ELi4096ELb0ELi4ELb1EEEvNS_4PlanE",
+    "k_fused_bf16_b4096_reduce": "_ZN4uzip7k_fusedILi0ELi4096ELb1ELi3ELb0EEEvNS_4PlanE",
     "k_decode_bf16": "_ZN4uzip8k_decodeILi0EEEvPKhmPhmNS_7CodecWsEPi",
     "k_hist_bf16": "_ZN4uzip6k_histILi0EEEvNS_4PlanE",
 }
