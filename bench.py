@@ -8,7 +8,7 @@ SURVEY 8(d)), plus the compression ratio.
 
 N = 1 workload "c2_shard_codec_roundtrip": one step = the single-GPU part of
 BASELINE configs[1] -- the 1 GiB bf16 N(0, 0.02) weight shard compressed
-(uzip_compress: k_table + k_encode, rows a1-a5) and decompressed
+(uzip_compress: k_hist + k_norm + k_fused, rows a1-a5) and decompressed
 (uzip_decompress: k_decode, rows a7-a8) through the C ABI.  Inputs (1 GiB) are
 larger than L2 (126 MB), so no flush is needed between steps.
 

@@ -276,7 +276,7 @@ int occupancy(K kernel, int threads, size_t smem) {
 template <int DT>
 cudaError_t launch_decode_t(const void *in, uint64_t in_bytes, void *out, uint64_t n, void *ws_ptr,
                             int32_t *d_status, cudaStream_t st, int max_ctas, uint64_t est_blocks) {
-  CodecWs ws = CodecWs::carve(ws_ptr, 0);
+  CodecWs ws = CodecWs::carve(ws_ptr);
   auto kern = k_decode<DT>;
   static bool attr = false;
   if (!attr) {

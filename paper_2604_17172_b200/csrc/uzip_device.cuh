@@ -88,38 +88,16 @@ struct StreamGeom {
   }
 };
 
-// Workspace carve-up (host and device agree; control words first).
+// Decoder control words at the start of the caller's workspace (uzip_decompress): the first error
+// and the CTA arrival counter, both reset by the last CTA (the encoder's workspace is EncWs, plan.h).
 struct CodecWs {
-  uint32_t *ticket;       // k_encode tile ticket (zeroed by k_table)
   uint32_t *err;          // k_decode first error (self-resetting)
   uint32_t *dec_arrive;   // k_decode CTA arrivals (self-resetting)
-  uint32_t *arrive;       // k_table per-chunk arrivals (self-resetting)
-  uint32_t *counts;       // k_table per-chunk histogram (self-resetting)
-  uint4 *enc;             // per-chunk encode tables {rcp, f<<19|shift, bias, M-f}
-  unsigned long long *tile_status;  // look-back words (zeroed by k_table)
-
-  __host__ __device__ static uint64_t bytes_for(uint64_t n_chunks, uint64_t n_tiles) {
-    uint64_t b = 64;                       // control words
-    b += round16(4 * n_chunks);            // arrive
-    b += 1024 * n_chunks;                  // counts
-    b += 4096 * n_chunks;                  // enc
-    b += 8 * n_tiles;                      // tile status
-    return round16(b);
-  }
-  __host__ __device__ static CodecWs carve(void *base, uint64_t n_chunks) {
+  __host__ __device__ static CodecWs carve(void *base) {
     CodecWs w;
     uint8_t *p = (uint8_t *)base;
-    w.ticket = (uint32_t *)(p + 0);
     w.err = (uint32_t *)(p + 4);
     w.dec_arrive = (uint32_t *)(p + 8);
-    p += 64;
-    w.arrive = (uint32_t *)p;
-    p += round16(4 * n_chunks);
-    w.counts = (uint32_t *)p;
-    p += 1024 * n_chunks;
-    w.enc = (uint4 *)p;
-    p += 4096 * n_chunks;
-    w.tile_status = (unsigned long long *)p;
     return w;
   }
 };
