@@ -3,7 +3,7 @@
 // Host side only: it lays out the symmetric region every rank exports
 // (staging slots, tile flags, credits), maps the peers' regions (CUDA IPC
 // between processes, direct pointers in single-process mode), and turns each
-// call into rounds of at most one staging slot, each round = k_table + one
+// call into rounds of at most one staging slot, each round = k_hist + k_norm + one
 // k_fused launch (fused.cu).  No host synchronization on the data path.
 //
 // Paper: split-send P2P, compress-on-send / decompress-

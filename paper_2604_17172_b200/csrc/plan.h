@@ -41,8 +41,8 @@ struct EncJob {
   unsigned long long *flag[kMaxRanks];      // tile flags at each destination (null: no flags)
   const unsigned long long *credit[kMaxRanks];  // local word: last epoch the destination consumed from this slot
   uint32_t epoch[kMaxRanks];                // flag epoch per destination (round sequence + 1)
-  uint4 *enc;                               // per-chunk encode entries (k_table)
-  uint16_t *tab16;                          // per-chunk serialized tables (k_table)
+  uint4 *enc;                               // per-chunk encode entries (k_norm)
+  uint16_t *tab16;                          // per-chunk serialized tables (k_norm)
   unsigned long long *tile_status;          // per-tile look-back words (zeroed by k_hist)
   uint32_t *partial;                        // k_hist partial histograms [chunk][kMaxHistParts][256]
   uint64_t *d_out_bytes;                    // codec: stream size (may be null)
