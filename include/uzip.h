@@ -56,7 +56,9 @@ typedef enum {
   UZIP_ERR_CORRUPT_STREAM = 4,    /* async: header, table, directory or block check failed  */
   UZIP_ERR_SIZE_MISMATCH = 5,     /* async: stream n/dtype differ from the call's           */
   UZIP_ERR_CUDA = 6,              /* a CUDA runtime call failed                              */
-  UZIP_ERR_COMM = 7,              /* communicator setup / bootstrap failure                 */
+  UZIP_ERR_COMM = 7,              /* communicator setup / bootstrap failure; a call that    */
+                                  /* needs co-scheduled co-resident ranks under serialised  */
+                                  /* kernel execution (see uzip_comm_init_all)              */
   UZIP_ERR_TIMEOUT = 8,           /* async: a peer flag did not arrive in poll_timeout_ms   */
   UZIP_ERR_NOT_IMPLEMENTED = 9
 } uzip_status_t;
@@ -93,7 +95,8 @@ UZIP_API uzip_status_t uzip_workspace_init(void *ws, size_t ws_bytes, void *stre
  * (Steps 1-3 of P:159-170 fused as in P:317-376: split + sampled per-chunk
  * tables + warp-per-block rANS + look-back compaction, no coalescing pass).
  * `out_capacity` must be >= uzip_compress_bound.  The stream's byte count is
- * written to the device word *d_out_bytes when the stream work completes.
+ * written to the device word *d_out_bytes when the stream work completes
+ * (0 = an internal kernel failure; a valid stream is at least 64 bytes).
  * Output bytes equal the CPU oracle's for the same input and params. */
 UZIP_API uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, void *out,
                             size_t out_capacity, uint64_t *d_out_bytes, void *ws, size_t ws_bytes,
@@ -122,7 +125,7 @@ typedef int (*uzip_allgather_fn)(const void *send, void *recv, size_t bytes_per_
  *  min_compress_bytes  compress only messages >= this (R10; default 1 MiB)
  *  staging_bytes       receive staging per peer = 2 slots, bounds the footprint (default 512 MiB)
  *  pipe_chunk_bytes    largest round (one UZB1 stream) in input bytes (P:249-252 large blocks;
- *                      default: as large as a slot allows)
+ *                      default: as large as a slot allows; rounded down to a multiple of 16)
  *  max_ctas            CTAs of each fused kernel (0 = all SMs); loopback tests use small values
  *  poll_timeout_ms     peer-flag wait bound before UZIP_ERR_TIMEOUT (default 10000)
  *  codec               stream parameters used on the wire */
@@ -147,7 +150,14 @@ UZIP_API uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, i
  * share a GPU (here, or IPC ranks whose GPU UUIDs match) run their persistent
  * kernels side by side: a launch whose decode items spin on a peer holds at
  * most 1/k of the CTA slots for k co-resident ranks, and slot credits are
- * always awaited by a one-thread kernel, so every producer finds an SM. */
+ * always awaited by a one-thread kernel, so every producer finds an SM.
+ * Serialised execution (CUDA_LAUNCH_BLOCKING=1, a kernel profiler such as
+ * ncu, or UZIP_SERIALIZED=1) runs one kernel at a time, so co-resident ranks
+ * can only exchange data whose producer launch finishes before the consumer
+ * launch starts: a send/recv of at most two staging slots.  Any other call
+ * between co-resident ranks (a launch that both encodes for and decodes from
+ * peers, a relay, or a round that waits for a slot credit) returns
+ * UZIP_ERR_COMM at once instead of spinning until poll_timeout_ms. */
 UZIP_API uzip_status_t uzip_comm_init_all(uzip_comm_t *comms, int nranks, const int *devices,
                                  const uzip_config_t *cfg);
 UZIP_API uzip_status_t uzip_comm_destroy(uzip_comm_t comm);

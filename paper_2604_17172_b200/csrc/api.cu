@@ -83,6 +83,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   p.ticket = reinterpret_cast<uint32_t *>(w + 16);
   p.err = reinterpret_cast<uint32_t *>(w + 24);
   p.timeout_ns = 10000000000ull;
+  p.codec_call = 1;
   EncJob &J = p.e[0];
   J.in = static_cast<const uint8_t *>(in);
   J.g = g;

@@ -255,15 +255,21 @@ __global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__
 
 // ================================================================ launchers
 namespace {
+constexpr int kMaxDev = 64;
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDev ? dev : 0;
+}
 int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[kMaxDev] = {0};
+  const int dev = cur_dev();
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
 }
 
 template <typename K>
@@ -278,10 +284,12 @@ cudaError_t launch_decode_t(const void *in, uint64_t in_bytes, void *out, uint64
                             int32_t *d_status, cudaStream_t st, int max_ctas, uint64_t est_blocks) {
   CodecWs ws = CodecWs::carve(ws_ptr);
   auto kern = k_decode<DT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecShared::kBytes);
-    attr = true;
+  static bool attr[kMaxDev] = {false};  // per device
+  const int dev = cur_dev();
+  if (!attr[dev]) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecShared::kBytes);
+    if (e != cudaSuccess) return e;
+    attr[dev] = true;
   }
   int grid = sm_count() * occupancy(kern, 256, DecShared::kBytes);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;

@@ -88,6 +88,8 @@ uzip_config_t resolve_cfg(const uzip_config_t *in) {
   if (c.min_compress_bytes == ~0ull) c.min_compress_bytes = ~0ull;  // never compress
   if (!c.staging_bytes) c.staging_bytes = env("UZIP_STAGING_BYTES", 512ull << 20);
   if (!c.pipe_chunk_bytes) c.pipe_chunk_bytes = env("UZIP_PIPE_CHUNK_BYTES", ~0ull);
+  // rounds start at multiples of the pipe chunk: keep them 16-byte aligned for the 128-bit raw path
+  c.pipe_chunk_bytes = std::max<uint64_t>(16, c.pipe_chunk_bytes & ~15ull);
   if (!c.max_ctas) c.max_ctas = (uint32_t)env("UZIP_MAX_CTAS", 0);
   if (!c.poll_timeout_ms) c.poll_timeout_ms = (uint32_t)env("UZIP_POLL_TIMEOUT_MS", 10000);
   return c;
@@ -170,6 +172,21 @@ uint64_t round_elems(uzip_comm *c, int dt, bool compressed, uint64_t count, Stre
     else hi = k - 1;
   }
   return lo * unit;
+}
+
+// Serialised kernel execution (CUDA_LAUNCH_BLOCKING=1, a kernel profiler, or the explicit knob):
+// kernels of co-resident ranks can no longer run side by side (uzip.h, uzip_comm_init_all).
+bool serialized_env() {
+  static const int v = [] {
+    const char *k = getenv("UZIP_SERIALIZED");
+    if (k) return atoi(k) != 0 ? 1 : 0;
+    const char *b = getenv("CUDA_LAUNCH_BLOCKING");
+    if (b && atoi(b) != 0) return 1;
+    const char *inj = getenv("CUDA_INJECTION64_PATH");  // ncu / nsys inject a library into the target
+    if (inj && (strstr(inj, "nsight") || strstr(inj, "Nsight") || strstr(inj, "ncu"))) return 1;
+    return 0;
+  }();
+  return v != 0;
 }
 
 bool compress_message(uzip_comm *c, uint64_t message_bytes) { return message_bytes >= c->cfg.min_compress_bytes; }
@@ -279,7 +296,23 @@ void fwd_setup(uzip_comm *c, Plan &p, int j, const std::vector<int> &dsts) {
   }
 }
 
+// A launch that can only finish while a co-resident peer's launch runs at the same time: it both
+// encodes for and decodes from peers, relays, or reuses a slot whose credit a later consumer
+// launch releases.
+bool needs_coscheduling(const Plan &p) {
+  bool remote_src = false, fwd = false, credit = false;
+  for (int j = 0; j < p.nd_jobs; ++j) {
+    remote_src |= p.d[j].nsrc > (p.d[j].me >= 0 ? 1u : 0u);
+    fwd |= p.d[j].nfwd > 0;
+    for (uint32_t d = 0; d < p.d[j].nfwd; ++d) credit |= p.d[j].fepoch[d] > 2;
+  }
+  for (int j = 0; j < p.ne; ++j)
+    for (uint32_t d = 0; d < p.e[j].nd; ++d) credit |= p.e[j].credit[d] && p.e[j].epoch[d] > 2;
+  return (p.ne > 0 && remote_src) || fwd || credit;
+}
+
 uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
+  if (c->share > 1 && serialized_env() && needs_coscheduling(p)) return UZIP_ERR_COMM;  // fail fast, no hang
   for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
   for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += items_of(p.d[j]);
   p.n_c_items = p.has_copy ? p.c.ntiles : 0;
@@ -644,6 +677,11 @@ uzip_status_t uzip_alltoall(const void *sendbuf, void *recvbuf, size_t count, uz
   const uint32_t eb = elem_bytes(dt);
   const int N = c->nranks, me = c->rank;
   if (N > 1 && (count * eb) % 16 != 0) return UZIP_ERR_INVALID_ARG;  // 16-byte aligned per-peer chunks
+  {  // out of place only: E items read chunk d of sendbuf while D items write chunk s of recvbuf
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(sendbuf), b0 = reinterpret_cast<uintptr_t>(recvbuf);
+    const uint64_t len = (uint64_t)N * count * eb;
+    if (a0 < b0 + len && b0 < a0 + len) return UZIP_ERR_INVALID_ARG;
+  }
   const uint64_t msg = (uint64_t)N * count * eb;                       // R10: the user message
   const bool comp = compress_message(c, msg);
   cudaStream_t st = (cudaStream_t)stream;

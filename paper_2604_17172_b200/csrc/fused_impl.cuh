@@ -1290,21 +1290,33 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
     if (atomicAdd(P.ticket + 1, 1u) == gridDim.x - 1) {
       P.ticket[0] = 0;
       P.ticket[1] = 0;
+      if (P.codec_call) {  // uzip_compress: the error word is private to this call
+        if (ld_volatile_u32(P.err))
+          for (int j = 0; j < P.ne; ++j)
+            if (P.e[j].d_out_bytes) *P.e[j].d_out_bytes = 0;
+        P.err[0] = 0;
+      }
       __threadfence();
     }
   }
 }
 
 // ================================================================ launchers
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
 inline int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[kMaxDevices] = {0};
+  const int dev = current_device();
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
 }
 
 template <int DT>
@@ -1333,10 +1345,12 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
   const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0);
   auto kern = k_fused<DT, B, RED, MINB, DONLY>;
-  static int attr_set = 0;
-  if (attr_set < C::smem(true, RED)) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(true, RED));
-    attr_set = C::smem(true, RED);
+  static int attr_set[kMaxDevices] = {0};  // the attribute applies per device
+  const int dev = current_device();
+  if (attr_set[dev] < C::smem(true, RED)) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(true, RED));
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = C::smem(true, RED);
   }
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);

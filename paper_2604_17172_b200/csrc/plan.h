@@ -100,6 +100,8 @@ struct Plan {
   uint32_t credit_ready;                    // 1: k_credit already waited for every slot credit of this launch
   uint32_t share;                           // ranks whose kernels share this GPU (loopback / co-located processes)
   float *acc;                               // reduce: fp32 accumulators, B floats per (CTA, warp) (L2-resident)
+  uint32_t codec_call;                      // 1: uzip_compress -- the last CTA out reports an internal
+                                            // failure as *d_out_bytes = 0 and clears the error word
 };
 
 // Slot credits one launch needs (a12), waited for by k_credit -- one thread --

@@ -48,3 +48,35 @@ def test_protocol_under_random_delays():
            "p2p_many_rounds or allgather or allreduce or broadcast or alltoall or reduce_scatter"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+_SERIAL_SCRIPT = r"""
+import sys, time
+sys.path.insert(0, %(root)r)
+import torch
+import __graft_entry__ as g
+import paper_2604_17172_b200 as uz
+g.smoke()  # codec round trip + one P2P round: no co-scheduled kernels needed
+comms = uz.Comm.init_all(2, [0, 0], min_compress_bytes=1, staging_bytes=16 << 20)
+x = torch.zeros(1 << 20, dtype=torch.bfloat16, device="cuda")
+t0 = time.time()
+try:
+    comms[0].all_reduce(torch.empty_like(x), x)
+    raise SystemExit("allreduce between co-resident ranks was not refused under serialisation")
+except uz.UzipError as e:
+    assert e.status == uz.ERR_COMM, e
+assert time.time() - t0 < 5, "the refusal must not wait for a poll timeout"
+print("serialized ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"CUDA_LAUNCH_BLOCKING": "1"}, {"UZIP_SERIALIZED": "1"}])
+def test_serialized_execution_fails_fast(env):
+    """Serialised kernels (CUDA_LAUNCH_BLOCKING, ncu): smoke() still passes and a collective between
+    co-resident ranks returns UZIP_ERR_COMM at once instead of a poll timeout."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, "-c", _SERIAL_SCRIPT % {"root": ROOT}], capture_output=True, text=True,
+                       timeout=300, cwd=ROOT, env=dict(os.environ, **env))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "smoke ok" in r.stdout and "serialized ok" in r.stdout
