@@ -78,6 +78,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   // one encode job, one destination (the caller's stream buffer), no flags
   Plan p;
   memset(&p, 0, sizeof p);
+  p.ag_job = -1;
   p.dtype = (int)dtype;
   uint8_t *w = static_cast<uint8_t *>(ws);
   p.ticket = reinterpret_cast<uint32_t *>(w + 16);

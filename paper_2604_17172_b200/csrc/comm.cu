@@ -193,6 +193,7 @@ bool compress_message(uzip_comm *c, uint64_t message_bytes) { return message_byt
 
 void base_plan(uzip_comm *c, Plan &p, int dt) {
   memset(&p, 0, sizeof p);
+  p.ag_job = -1;
   p.dtype = dt;
   p.ticket = ws_ticket(c);
   p.err = reinterpret_cast<uint32_t *>(c->region);
@@ -306,7 +307,7 @@ bool needs_coscheduling(const Plan &p) {
     fwd |= p.d[j].nfwd > 0;
     for (uint32_t d = 0; d < p.d[j].nfwd; ++d) credit |= p.d[j].fepoch[d] > 2;
   }
-  for (int j = 0; j < p.ne; ++j)
+  for (int j = 0; j < p.ne + (p.ag_job >= 0 ? 1 : 0); ++j)
     for (uint32_t d = 0; d < p.e[j].nd; ++d) credit |= p.e[j].credit[d] && p.e[j].epoch[d] > 2;
   return (p.ne > 0 && remote_src) || fwd || credit;
 }
@@ -334,7 +335,7 @@ uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
   if (!first_rounds || (UZIP_SHARED_CREDIT_KERNEL && c->share > 1)) {
     CreditWait w;
     memset(&w, 0, sizeof w);
-    for (int j = 0; j < p.ne; ++j)
+    for (int j = 0; j < p.ne + (p.ag_job >= 0 ? 1 : 0); ++j)  // + the fused allgather stream
       for (uint32_t d = 0; d < p.e[j].nd; ++d)
         if (p.e[j].credit[d] && p.e[j].epoch[d] > 2 && w.n < 2 * kMaxRanks) {
           w.cr[w.n] = p.e[j].credit[d];
@@ -655,6 +656,55 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
   // threshold applies to the user message (R10) in both phases.
   const uint64_t saved = c->cfg.min_compress_bytes;
   const bool comp = compress_message(c, count * eb);
+  static const bool fused = !(getenv("UZIP_AR_FUSED") && atoi(getenv("UZIP_AR_FUSED")) == 0);
+  if (comp && N > 1 && fused && !c->cfg.codec.global_table) {
+    // One pass per round (a9, R26): one launch holds the reduce-scatter streams (E items), the reduce
+    // items -- which round each reduced tile and code it straight into the allgather stream to the
+    // N-1 peers (no HBM round trip, no second table pass) -- and the decoders of the peers'
+    // allgather streams.  Its per-chunk tables are sampled from each chunk's first tile.
+    const int dt = (int)dtype, me = c->rank;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (uzip_status_t s2 = begin_call(c, 2ull * (N - 1) * shard * eb, true, st)) return s2;
+    if (uzip_status_t s2 = ensure_acc(c)) return s2;
+    const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
+    uint8_t *out = static_cast<uint8_t *>(recvbuf);
+    const uint64_t per = round_elems(c, dt, true, shard, nullptr);
+    const std::vector<int> peers = peers_from(c);
+    std::vector<int> all;
+    for (int r = 0; r < N; ++r) all.push_back(r);
+    for (uint64_t o = 0; o < shard; o += per) {
+      const uint64_t n = std::min<uint64_t>(per, shard - o);
+      Plan p;
+      base_plan(c, p, dt);
+      int j = 0;
+      for (int d : peers) {  // shard d of my input -> its owner (reduce-scatter streams)
+        enc_job(c, p, j, dt, in + ((uint64_t)d * shard + o) * eb, n, true, {d});
+        ++j;
+      }
+      uint8_t *mine = out + ((uint64_t)me * shard + o) * eb;
+      dec_job(c, p, 0, dt, n, true, all, me, in + ((uint64_t)me * shard + o) * eb, mine);
+      p.d[0].op = (uint32_t)op;
+      // single tiles per reduce item: the re-encoded tiles finish their look-back in tile order, so
+      // runs of consecutive tiles per CTA would chain the CTAs (measured 4x slower at N = 2)
+      p.d[0].run = 1;
+      // the allgather stream of my reduced shard: e[N-1], no E items of its own (p.ne stays N-1)
+      const int ne = p.ne;
+      enc_job(c, p, ne, dt, mine, n, true, peers);
+      p.ne = ne;
+      p.ag_job = ne;
+      uzip_codec_params_t cp = c->cfg.codec;
+      resolve_geom(dt, n, &cp, &p.e[ne].g);
+      cp.sample_symbols = kTileBlocks * p.e[ne].g.B;  // R26: the chunk's first tile is its sample
+      resolve_geom(dt, n, &cp, &p.e[ne].g);
+      j = 1;
+      for (int s : peers) {  // the peers' reduced shards
+        dec_job(c, p, j, dt, n, true, {s}, -1, nullptr, out + ((uint64_t)s * shard + o) * eb);
+        ++j;
+      }
+      if (uzip_status_t s2 = launch(c, p, true, st)) return s2;
+    }
+    return UZIP_OK;
+  }
   uzip_status_t s = begin_call(c, 0, comp, (cudaStream_t)stream);
   if (s != UZIP_OK) return s;
   c->cfg.min_compress_bytes = comp ? 0 : ~0ull;

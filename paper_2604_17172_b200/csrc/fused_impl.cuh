@@ -35,7 +35,7 @@
 #define UZIP_ENC_GROUP 4  // encoder rounds whose symbols/table entries are loaded ahead
 #endif
 #ifndef UZIP_RED_MINB
-#define UZIP_RED_MINB 3   // resident CTAs per SM targeted by reduce launches (accumulators in L2, not smem)
+#define UZIP_RED_MINB 2   // resident CTAs per SM targeted by reduce launches (r02: 2 without spills beats 3 with)
 #endif
 #ifndef UZIP_ENC_MINB
 #define UZIP_ENC_MINB 3   // resident CTAs per SM targeted by launches with encode items (measured)
@@ -69,6 +69,11 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
     const uint64_t nctas = (uint64_t)gridDim.x * gridDim.y;
     const uint64_t me = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
     for (uint64_t t = me * kHistThreads + tid; t < tiles_of(g); t += nctas * kHistThreads) J.tile_status[t] = 0ull;
+    if (P.ag_job >= 0 && blockIdx.z == 0) {  // ... and those + the table flags of the fused allgather stream
+      const EncJob &A = P.e[P.ag_job];
+      for (uint64_t t = me * kHistThreads + tid; t < tiles_of(A.g); t += nctas * kHistThreads) A.tile_status[t] = 0ull;
+      for (uint64_t c2 = me * kHistThreads + tid; c2 < A.g.n_chunks; c2 += nctas * kHistThreads) A.partial[c2] = 0u;
+    }
   }
   if (c >= g.n_chunks) return;
   const uint32_t len = g.sample_len(c), parts = hist_parts(len);
@@ -113,24 +118,15 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
   J.partial[((uint64_t)c * kMaxHistParts + part) * 256 + tid] = sum;
 }
 
-template <int DT>
-__global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
-  __shared__ uint32_t cnt[256];
-  __shared__ unsigned long long red64[8];
-  __shared__ uint32_t red32[8];
-  const EncJob &J = P.e[blockIdx.y];
-  if (J.raw) return;
-  const StreamGeom &g = J.g;
+// a3, all 256 threads of a CTA: thread s holds cnt = count of symbol s in the chunk's sample; rule
+// N1 (R5) -> the chunk's encode entries (enc, global), its 512-byte serialized table (tab16, global)
+// and, if `tab` is not null, the entries in shared memory too.  red64/red32: 8 words of smem scratch.
+__device__ __forceinline__ void norm_tables(uint32_t cnt, uint4 *enc, uint16_t *tab16, uint4 *tab,
+                                            unsigned long long *red64, uint32_t *red32) {
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  const uint32_t c = blockIdx.x;
-  if (c >= g.n_chunks) return;
-  const uint32_t parts = hist_parts(g.sample_len(c));
-  uint32_t sum = 0;
-  for (uint32_t p = 0; p < parts; ++p) sum += J.partial[((uint64_t)c * kMaxHistParts + p) * 256 + tid];
-  cnt[tid] = sum;
   // ---- rule N1 (R5): total and argmax (lowest symbol on ties): key = cnt<<8 | (255 - s)
-  unsigned long long key = ((unsigned long long)cnt[tid] << 8) | (255u - tid);
-  unsigned long long tot = cnt[tid];
+  unsigned long long key = ((unsigned long long)cnt << 8) | (255u - tid);
+  unsigned long long tot = cnt;
   for (int o = 16; o; o >>= 1) {
     unsigned long long ok = __shfl_xor_sync(0xFFFFFFFFu, key, o);
     key = ok > key ? ok : key;
@@ -149,7 +145,7 @@ __global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
   const uint32_t best = 255u - (uint32_t)(best_key & 0xFFu);
   uint32_t f;
   if (total == 0) f = kM / 256;
-  else f = 1u + (uint32_t)(((unsigned long long)cnt[tid] * (kM - 256)) / total);
+  else f = 1u + (uint32_t)(((unsigned long long)cnt * (kM - 256)) / total);
   __syncthreads();
   uint32_t fs = f;
   for (int o = 16; o; o >>= 1) fs += __shfl_xor_sync(0xFFFFFFFFu, fs, o);
@@ -169,8 +165,27 @@ __global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
   uint32_t woff = 0;
   for (int w = 0; w < warp; ++w) woff += red32[w];
   const uint32_t cdf = woff + incl - f;
-  J.enc[c * 256 + tid] = make_enc_entry(f, cdf);
-  J.tab16[c * 256 + tid] = (uint16_t)f;
+  const uint4 ent = make_enc_entry(f, cdf);
+  enc[tid] = ent;
+  tab16[tid] = (uint16_t)f;
+  if (tab) tab[tid] = ent;
+  __syncthreads();  // red32 / red64 free again; tab complete
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
+  __shared__ unsigned long long red64[8];
+  __shared__ uint32_t red32[8];
+  const EncJob &J = P.e[blockIdx.y];
+  if (J.raw) return;
+  const StreamGeom &g = J.g;
+  const int tid = threadIdx.x;
+  const uint32_t c = blockIdx.x;
+  if (c >= g.n_chunks) return;
+  const uint32_t parts = hist_parts(g.sample_len(c));
+  uint32_t sum = 0;
+  for (uint32_t p = 0; p < parts; ++p) sum += J.partial[((uint64_t)c * kMaxHistParts + p) * 256 + tid];
+  norm_tables(sum, J.enc + c * 256, J.tab16 + c * 256, nullptr, red64, red32);
 }
 
 // ================================================================ shared pieces
@@ -238,6 +253,26 @@ static __device__ bool wait_credit(const Plan &P, const unsigned long long *cr, 
       }
     }
     __nanosleep(64);
+  }
+}
+
+// Poll a 32-bit flag until it equals `want` (gpu scope: a flag of this launch on this GPU).
+static __device__ bool wait_u32(const Plan &P, const uint32_t *f, uint32_t want, unsigned long long &seen) {
+  unsigned long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    const uint32_t v = ld_acquire_gpu_u32(f);
+    if (v == want) return true;
+    if ((spin & 63) == 63) {
+      if (ld_volatile_u32(P.err)) return false;
+      const unsigned long long now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > P.timeout_ns) {
+        seen = v;
+        raise_err_at(P, UZIP_ERR_TIMEOUT, 5, want, v, (uint64_t)(uintptr_t)f);
+        return false;
+      }
+    }
+    __nanosleep(32);
   }
 }
 
@@ -378,6 +413,7 @@ struct FusedShared {
   unsigned long long src_off[kMaxRanks];
   unsigned long long src_payload[kMaxRanks];
   uint32_t red[kWarps];
+  unsigned long long red64[kWarps];
 };
 
 // ---------------------------------------------------------------- E item
@@ -427,7 +463,7 @@ static __device__ void finalize_stream(const EncJob &J, unsigned long long paylo
 // (R-1-j)*32, lanes in order within a row) for the encoder; otherwise element
 // order (the stored-raw payload).  RES: also store the residual plane(s) to
 // every destination (split-send: they leave before the exponents are coded).
-template <int DT, int B, bool RES, bool REV, bool ND1>
+template <int DT, int B, bool RES, bool REV, bool ND1, bool COH = false>
 __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
                                               uint8_t *buf) {
   using C = FusedCfg<DT, B>;
@@ -443,7 +479,9 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
   for (int h = 0; h < C::kIters; h += C::kBatch) {
     uint4 v[C::kBatch];
 #pragma unroll
-    for (int i = 0; i < C::kBatch; ++i) v[i] = ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
+    for (int i = 0; i < C::kBatch; ++i)
+      v[i] = COH ? ld_cg_v4(src + (size_t)(lane + 32 * (h + i)) * 16)   // written earlier in this launch
+                 : ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
 #pragma unroll
     for (int i = 0; i < C::kBatch; ++i) {
       const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;  // element within block
@@ -492,11 +530,43 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
   }
 }
 
-template <int DT, int B, bool RES, bool REV>
+template <int DT, int B, bool RES, bool REV, bool COH = false>
 __device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
                                             uint8_t *buf) {
-  if (!RES || J.nd == 1) split_block_t<DT, B, RES, REV, true>(J, g, b, src, buf);
-  else split_block_t<DT, B, RES, REV, false>(J, g, b, src, buf);
+  if (!RES || J.nd == 1) split_block_t<DT, B, RES, REV, true, COH>(J, g, b, src, buf);
+  else split_block_t<DT, B, RES, REV, false, COH>(J, g, b, src, buf);
+}
+
+// a1 for one 16-byte vector of block b that is already in registers (the reduced output of the fused
+// allreduce, a9): its symbols go to the encoder's row layout in buf (coding order, as split_block
+// with REV), its residual bytes to every destination's residual plane(s).  e = first element.
+template <int DT, int B>
+__device__ __forceinline__ void split_vec(const EncJob &J, const StreamGeom &g, uint64_t b, uint32_t e, uint4 v,
+                                          uint8_t *buf) {
+  static_assert(DT == kBF16 || DT == kF16 || DT == kF32, "reduced dtypes (R22)");
+  uint8_t *sp = buf + (uint32_t)(B - 32) - (e & ~31u) + (e & 31u);
+  if (DT == kF32) {
+    uint32_t s4, h4;
+    uint2 lo;
+    split4_f32(v, s4, lo, h4);
+    *reinterpret_cast<uint32_t *>(sp) = s4;
+    for (uint32_t d = 0; d < J.nd; ++d) {
+      *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + 2 * (b * B + e)) = lo;
+      *reinterpret_cast<uint32_t *>(J.dst[d] + g.off_res1 + b * B + e) = h4;
+    }
+  } else {
+    uint32_t s0, s1, q0, q1;
+    if (DT == kBF16) {
+      split4_bf16(v.x, v.y, s0, q0);
+      split4_bf16(v.z, v.w, s1, q1);
+    } else {
+      split4_f16(v.x, v.y, s0, q0);
+      split4_f16(v.z, v.w, s1, q1);
+    }
+    *reinterpret_cast<uint2 *>(sp) = make_uint2(s0, s1);
+    for (uint32_t d = 0; d < J.nd; ++d)
+      *reinterpret_cast<uint2 *>(J.dst[d] + g.off_res0 + b * B + e) = make_uint2(q0, q1);
+  }
 }
 
 // a4: 32 interleaved rANS lanes, rounds R-1 .. 0 (branch-free body); the
@@ -628,78 +698,45 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
   __syncthreads();  // the ring and the pending sizes are free again
 }
 
-// One encode tile: every warp codes one block; one warp finds the tile's
-// offset by decoupled look-back over tiles; the last warp of the tile to
-// finish its stores releases the tile's flags.
-template <int DT, int B>
-static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &enc_key, uint32_t &credit_done, uint8_t *ring, int ring_bytes, EncPending &pd,
-                         uint64_t next_it) {
+// The destinations' slots of encode job jidx are free (a12): the first tile of the job in this CTA
+// waits for their credits (or for k_credit, which waited already).  CTA-uniform; false = abort.
+static __device__ bool credit_gate(const Plan &P, const EncJob &J, int jidx, uint32_t &credit_done, FusedShared &S) {
+  if ((credit_done >> jidx) & 1u) return true;
+  if (threadIdx.x == 0) {
+    uint32_t ok = 1;
+    if (P.credit_ready) ok = ld_volatile_u32(P.err) == 0;  // k_credit waited (or failed)
+    else
+      for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
+    S.abort = ok ? 0u : 1u;
+  }
+  __syncthreads();
+  if (S.abort) return false;
+  credit_done |= 1u << jidx;
+  return true;
+}
+
+// a4-a6 for one tile whose blocks are split (symbols in each warp's buffer, residual stored): code
+// every block (one warp each), park the coded tile or find its offset by look-back, store it to every
+// destination, release the tile flags.  `src` is the tile's input, re-read for stored-raw blocks and
+// the rare overflow path (COH: written earlier in this launch -- the fused allreduce's reduced shard).
+template <int DT, int B, bool COH>
+static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem,
+                                 FusedShared &S, uint8_t *ring, int ring_bytes, EncPending &pd, const uint8_t *in) {
   using C = FusedCfg<DT, B>;
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  (void)next_it;  // an L2 prefetch of the next tile by warp 0 was measured slower (r1: 0.784 vs 0.754 ms/GiB)
-  if (!((credit_done >> jidx) & 1u)) {  // first tile of this job in this CTA (uniform)
-    if (tid == 0) {
-      uint32_t ok = 1;
-      if (P.credit_ready) ok = ld_volatile_u32(P.err) == 0;  // k_credit waited (or failed)
-      else
-        for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
-      S.abort = ok ? 0u : 1u;
-    }
-    __syncthreads();
-    if (S.abort) return;
-    credit_done |= 1u << jidx;
-  }
   bool flags = false;
   for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
-
-  if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
-    const uint64_t o0 = t * kRawTileBytes;
-    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
-    const uint64_t nv = len / 16;
-    for (uint64_t i = tid; i < nv; i += 256) {
-      const uint4 v = ldg_nc_v4(J.in + o0 + 16 * i);
-      for (uint32_t d = 0; d < J.nd; ++d) *reinterpret_cast<uint4 *>(J.dst[d] + o0 + 16 * i) = v;
-    }
-    for (uint64_t i = nv * 16 + tid; i < len; i += 256) {
-      const uint8_t v = J.in[o0 + i];
-      for (uint32_t d = 0; d < J.nd; ++d) J.dst[d][o0 + i] = v;
-    }
-    __syncthreads();
-    if (tid == 0 && flags) {
-      __threadfence_system();
-      for (uint32_t d = 0; d < J.nd; ++d)
-        if (J.flag[d]) {
-          stress_pause(P, t * 11 + d);
-          st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
-        }
-    }
-    return;
-  }
-
   const StreamGeom &g = J.g;
-  uint4 *tab = reinterpret_cast<uint4 *>(smem);
-  // One B-byte buffer per warp: symbol rows stored in coding order (round R-1
-  // first); the coded words grow from byte 0 into the rows already consumed.
+  const uint4 *tab = reinterpret_cast<const uint4 *>(smem);
   uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
   uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
   const uint64_t b0 = t * kTileBlocks;
   const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
-  const uint64_t key = ((uint64_t)jidx << 48) | c;
-  if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
-    tab[tid] = J.enc[c * 256 + tid];
-    enc_key = key;
-    __syncthreads();
-  }
-
   const uint64_t b = b0 + warp;
-  const uint8_t *src = J.in + b * (uint64_t)B * group_bytes(DT);
+  const uint8_t *src = in + b * (uint64_t)B * group_bytes(DT);
   uint32_t size = 0, kdir = 0, K = 0, x = kL;
   bool raw = false, ovf = false;
   if (b < g.n_blocks) {
-    // ---- a1: split; the residual goes straight to every destination (split-send)
-    split_block<DT, B, true, true>(J, g, b, src, buf);
-    __syncwarp();
     encode_block<DT, B, false>(J, g, 0, buf, tab, x, K, ovf);
     const uint32_t coded = (uint32_t)round16(128 + 2ull * K);
     raw = coded >= (uint32_t)B;  // stored raw (R13)
@@ -707,7 +744,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
     kdir = raw ? kRawBlock : K;
     __syncwarp();
     if (raw) {
-      split_block<DT, B, false, false>(J, g, b, src, buf);  // payload = the symbols in element order
+      split_block<DT, B, false, false, COH>(J, g, b, src, buf);  // payload = the symbols in element order
     } else if (!ovf && lane < 8) {
       buf16[K + lane] = 0;  // zero pad up to the 16-byte boundary (K + 8 <= kCap + 8 words fit)
     }
@@ -783,7 +820,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
       // rare: the words outran the consumed symbol rows -- code the block again,
       // now storing each word straight to its final place (offset known)
       __syncwarp();
-      split_block<DT, B, false, true>(J, g, b, src, buf);
+      split_block<DT, B, false, true, COH>(J, g, b, src, buf);
       __syncwarp();
       uint32_t x2 = kL, K2 = 0;
       bool o2 = false;
@@ -816,6 +853,66 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
       }
     }
   }
+}
+
+// One encode tile: every warp codes one block; one warp finds the tile's
+// offset by decoupled look-back over tiles; the last warp of the tile to
+// finish its stores releases the tile's flags.
+template <int DT, int B>
+static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
+                         uint64_t &enc_key, uint32_t &credit_done, uint8_t *ring, int ring_bytes, EncPending &pd,
+                         uint64_t next_it) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x, warp = warp_id();
+  (void)next_it;  // an L2 prefetch of the next tile by warp 0 was measured slower (r1: 0.784 vs 0.754 ms/GiB)
+  if (!credit_gate(P, J, jidx, credit_done, S)) return;
+  bool flags = false;
+  for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+
+  if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
+    const uint64_t o0 = t * kRawTileBytes;
+    const uint64_t len = min((uint64_t)kRawTileBytes, J.raw_bytes - o0);
+    const uint64_t nv = len / 16;
+    for (uint64_t i = tid; i < nv; i += 256) {
+      const uint4 v = ldg_nc_v4(J.in + o0 + 16 * i);
+      for (uint32_t d = 0; d < J.nd; ++d) *reinterpret_cast<uint4 *>(J.dst[d] + o0 + 16 * i) = v;
+    }
+    for (uint64_t i = nv * 16 + tid; i < len; i += 256) {
+      const uint8_t v = J.in[o0 + i];
+      for (uint32_t d = 0; d < J.nd; ++d) J.dst[d][o0 + i] = v;
+    }
+    __syncthreads();
+    if (tid == 0 && flags) {
+      __threadfence_system();
+      for (uint32_t d = 0; d < J.nd; ++d)
+        if (J.flag[d]) {
+          stress_pause(P, t * 11 + d);
+          st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
+        }
+    }
+    return;
+  }
+
+  const StreamGeom &g = J.g;
+  uint4 *tab = reinterpret_cast<uint4 *>(smem);
+  // One B-byte buffer per warp: symbol rows stored in coding order (round R-1
+  // first); the coded words grow from byte 0 into the rows already consumed.
+  uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t key = ((uint64_t)jidx << 48) | c;
+  if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
+    tab[tid] = J.enc[c * 256 + tid];
+    enc_key = key;
+    __syncthreads();
+  }
+  const uint64_t b = b0 + warp;
+  if (b < g.n_blocks) {
+    // ---- a1: split; the residual goes straight to every destination (split-send)
+    split_block<DT, B, true, true>(J, g, b, J.in + b * (uint64_t)B * group_bytes(DT), buf);
+    __syncwarp();
+  }
+  code_tile<DT, B, false>(P, J, jidx, t, smem, S, ring, ring_bytes, pd, J.in);
 }
 
 // ---------------------------------------------------------------- C item
@@ -1069,11 +1166,14 @@ struct FoldEpi {
 // ---------------------------------------------------------------- D item: decode + reduce (a9)
 template <int DT, int B>
 static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem, FusedShared &S,
-                         uint64_t &dec_key) {
+                         uint64_t &dec_key, uint64_t &enc_key, uint32_t &credit_done, uint8_t *ring, EncPending &pd) {
   using C = FusedCfg<DT, B>;
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   const StreamGeom &g = J.g;
   const uint32_t eb = elem_bytes(DT);
+  // fused allreduce (a9): this reduce job's tiles are also coded into the allgather stream e[ag_job]
+  const bool ag = jidx == 0 && P.ag_job >= 0 && !J.raw;
+  if (ag && !credit_gate(P, P.e[P.ag_job], P.ag_job, credit_done, S)) return;  // before the residual stores
 
   if (J.raw) {  // ---- below the threshold: fold raw tiles
     for (uint32_t s = 0; s < J.nsrc; ++s) {
@@ -1197,8 +1297,16 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     for (uint32_t e = lane * 8; e < (uint32_t)B; e += 256) {
       float a[8];
       acc_load8(acc + e, a);
-      *reinterpret_cast<uint4 *>(dst + e * eb) = narrow_vec<DT>(a);
-      if (DT == kF32) *reinterpret_cast<uint4 *>(dst + e * eb + 16) = narrow_vec<DT>(a + 4);
+      const uint4 v0 = narrow_vec<DT>(a);
+      *reinterpret_cast<uint4 *>(dst + e * eb) = v0;
+      uint4 v1 = v0;
+      if (DT == kF32) *reinterpret_cast<uint4 *>(dst + e * eb + 16) = v1 = narrow_vec<DT>(a + 4);
+      if constexpr (DT == kBF16 || DT == kF16 || DT == kF32) {
+        if (ag) {  // a1 of the allgather phase on the reduced values, still in registers
+          split_vec<DT, B>(P.e[P.ag_job], P.e[P.ag_job].g, b, e, v0, pay);
+          if (DT == kF32) split_vec<DT, B>(P.e[P.ag_job], P.e[P.ag_job].g, b, e + 4, v1, pay);
+        }
+      }
     }
   }
   __syncthreads();
@@ -1217,6 +1325,51 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
       if (DT == kF32) *reinterpret_cast<uint32_t *>(J.out + (g.n_coded + i) * eb) = r;
       else *reinterpret_cast<uint16_t *>(J.out + (g.n_coded + i) * eb) = (uint16_t)r;
     }
+  }
+  __syncthreads();
+  if (ag) {
+    const EncJob &A = P.e[P.ag_job];
+    const StreamGeom &ga = A.g;
+    const uint64_t ca = ga.n_blocks ? b0 / ga.CB : 0;
+    const uint64_t key = ((uint64_t)P.ag_job << 48) | ca;
+    uint4 *tab = reinterpret_cast<uint4 *>(smem);
+    uint32_t *tabflag = A.partial;  // per chunk: 1 = table published (reset by k_hist)
+    if (ga.n_blocks && b0 % ga.CB == 0) {
+      // the chunk's first tile is its sample (R26): histogram the symbols just split, rule N1, publish
+      uint32_t *hist = dtab;  // 8 x 256 counters in the decode-table region
+      dec_key = ~0ull;
+      for (int i = tid; i < kWarps * 256; i += 256) hist[i] = 0;
+      __syncthreads();
+      if (b < ga.n_blocks) {
+        uint32_t *h = hist + 256 * warp;
+        for (uint32_t i = lane; i < (uint32_t)B / 4; i += 32) {
+          const uint32_t w4 = reinterpret_cast<const uint32_t *>(pay)[i];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) atomicAdd(&h[(w4 >> (8 * k)) & 0xFFu], 1u);
+        }
+      }
+      __syncthreads();
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) cnt += hist[256 * w + tid];
+      norm_tables(cnt, A.enc + ca * 256, A.tab16 + ca * 256, tab, S.red64, S.red);
+      if (tid == 0) {
+        __threadfence();
+        st_release_gpu_u32(tabflag + ca, 1u);
+      }
+      enc_key = key;
+    } else if (ga.n_blocks && key != enc_key) {
+      if (tid == 0) {  // the chunk's first tile (a smaller ticket) publishes the table
+        unsigned long long v = 0;
+        S.abort = wait_u32(P, tabflag + ca, 1u, v) ? 0u : 1u;
+      }
+      __syncthreads();
+      if (S.abort) return;
+      tab[tid] = ld_cg_v4(A.enc + ca * 256 + tid);
+      enc_key = key;
+      __syncthreads();
+    }
+    code_tile<DT, B, true>(P, A, P.ag_job, t, smem, S, ring, P.ring_bytes, pd, A.in);
   }
   __syncthreads();
   dec_done(J);
@@ -1256,7 +1409,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
       const uint64_t r = Jd.run > 1 ? Jd.run : 1, t1 = min(Jd.ntiles, (k + 1) * r);
       for (uint64_t t = k * r; t < t1; ++t) {
         if constexpr (RED) {
-          if (Jd.nsrc > 1) red_item<DT, B>(P, Jd, j, t, smem, S, dec_key);
+          if (Jd.nsrc > 1) red_item<DT, B>(P, Jd, j, t, smem, S, dec_key, enc_key, credit_done, ring, pd);
           else dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);
         } else {
           dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);

@@ -102,6 +102,11 @@ struct Plan {
   float *acc;                               // reduce: fp32 accumulators, B floats per (CTA, warp) (L2-resident)
   uint32_t codec_call;                      // 1: uzip_compress -- the last CTA out reports an internal
                                             // failure as *d_out_bytes = 0 and clears the error word
+  // Fused allreduce (a9, R26): e[ag_job] (>= ne, so it has no E items of its own) is the allgather-phase
+  // stream of this rank's reduced shard.  The reduce items of job d[0] round each reduced tile and
+  // code it straight into that stream (one pass, no HBM round trip); the chunk's first tile samples
+  // the table (tabflag[c] = e[ag_job].partial[c] publishes it to the other tiles of the chunk).
+  int32_t ag_job;                           // -1: none
 };
 
 // Slot credits one launch needs (a12), waited for by k_credit -- one thread --

@@ -11,4 +11,4 @@ if [ -n "$BENCH" ]; then
   echo "bench rc=$?" >> gpurun_out/bench.log
 fi
 tail -40 gpurun_out/gpu_tests.log
-tail -5 gpurun_out/bench.log 2>/dev/null
+tail -5 gpurun_out/bench.log 2>/dev/null || true

@@ -730,3 +730,58 @@ def test_p2p_decode_runs(uz, chunk_blocks):
     finally:
         g.close()
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("nr", [2, 3])
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("codec", [dict(), dict(block_symbols=1024, chunk_blocks=16), dict(block_symbols=2048)])
+def test_allreduce_fused_wire_streams_equal_oracle(uz, orc, nr, dtype, codec):
+    """One-pass allreduce (a9, R26): every stream on the wire is the oracle's.  Reduce-scatter
+    phase: shard r of rank s's input, default sampling; allgather phase: rank s's REDUCED shard,
+    coded in the same launch as the reduction with each chunk's table sampled from its first tile
+    (sample_symbols = 8 B).  Outputs bit-exact against the fixed-order fold."""
+    g = Group(uz, nr, staging_bytes=64 << 20, min_compress_bytes=1, **codec)
+    try:
+        m = (1 << 20) + 4096 * 5 + 8 if dtype != F32 else (1 << 19) + 4096 * 3 + 4
+        ins = [gen("W", nr * m, 900 + 13 * r + dtype, dtype) for r in range(nr)]
+        xs = [dev(b, dtype) for b in ins]
+        outs = [torch.empty(nr * m, dtype=TD[dtype], device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_reduce(outs[r], xs[r], s))
+        ref = orc.allreduce(dtype, ins)
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], dtype), ref), r
+        B = codec.get("block_symbols", 4096)
+        for r in range(nr):
+            for s in range(nr):
+                if s == r:
+                    continue
+                rs = orc.compress(dtype, ins[s][r * m:(r + 1) * m], **codec)
+                assert g.comms[r].read_staging(s, 0, len(rs)) == rs, ("reduce-scatter stream", s, r)
+                ag = orc.compress(dtype, ref[s * m:(s + 1) * m], sample_symbols=8 * B, **codec)
+                assert g.comms[r].read_staging(s, 1, len(ag)) == ag, ("allgather stream", s, r)
+        st = g.comms[0].stats()
+        assert st["compressed"] and st["wire_bytes"] < st["raw_bytes"]
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("dist", ["W", "special"])
+def test_allreduce_fused_many_rounds_and_chunks(uz, orc, dist):
+    """The one-pass allreduce over many rounds (2 MiB slots: both slots of every pair are used by
+    each launch, so every round waits for the previous round's credits) and many table chunks per
+    round (chunk_blocks=8: every tile publishes its own table); incompressible (special) data
+    exercises stored-raw blocks of the re-encoded shard."""
+    nr = 3
+    g = Group(uz, nr, staging_bytes=4 << 20, min_compress_bytes=1, chunk_blocks=8)
+    try:
+        m = 3 * (1 << 20) + 4096 * 3 + 16
+        ins = [gen(dist, nr * m, 4400 + r, BF16) for r in range(nr)]
+        xs = [dev(b, BF16) for b in ins]
+        for it in range(2):
+            outs = [torch.empty(nr * m, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+            g.run(lambda r, c, s: c.all_reduce(outs[r], xs[r], s))
+            ref = orc.allreduce(BF16, ins)
+            for r in range(nr):
+                assert np.array_equal(host(outs[r], BF16), ref), (it, r)
+    finally:
+        g.close()
