@@ -269,3 +269,47 @@ def reduce_scatter(dtype: int, inputs, nranks: int, op: int = 0):
 
 def allreduce(dtype: int, inputs, op: int = 0):
     return reduce(dtype, inputs, op)
+
+
+# ---------------------------------------------------------------- O13 wire streams
+TILE_BLOCKS = 8  # blocks per tile of the GPU encoder (DESIGN R18); R26 samples one tile
+
+
+def wire_streams(kind: str, dtype: int, inputs, op: int = 0, **params):
+    """Which UZB1 streams a compressed single-round collective puts on the wire:
+    a list of (src, dst, phase, stream bytes).  Composed only of compress() and reduce() above.
+
+    p2p:        inputs = [x]: (0, 1, "p2p", compress(x)).
+    allgather:  the stream of in_r, sent to every peer.
+    reduce_scatter: for each j != r the stream of shard j of in_r, to rank j.
+    allreduce:  reduce_scatter's streams ("rs"), then the stream of rank j's reduced shard out_j to
+                every peer ("ag").  R26: the allgather phase is coded in the same pass
+                as the reduction, so each chunk's table is sampled from the chunk's first tile
+                (sample_symbols = 8 B) -- P:364's "first ... of each chunk", read at tile size.
+    """
+    N = len(inputs)
+    xs = [np.ascontiguousarray(a, dtype=NP_UINT[dtype]).reshape(-1) for a in inputs]
+    out = []
+    if kind == "p2p":
+        return [(0, 1, "p2p", compress(dtype, xs[0], **params))]
+    if kind == "allgather":
+        for r in range(N):
+            s = compress(dtype, xs[r], **params)
+            out += [(r, d, "ag", s) for d in range(N) if d != r]
+        return out
+    m = xs[0].size // N
+    for r in range(N):
+        for j in range(N):
+            if j != r:
+                out.append((r, j, "rs", compress(dtype, xs[r][j * m:(j + 1) * m], **params)))
+    if kind == "reduce_scatter":
+        return out
+    if kind != "allreduce":
+        raise ValueError(kind)
+    red = reduce(dtype, xs, op)
+    B = params.get("block_symbols") or 4096
+    agp = dict(params, sample_symbols=TILE_BLOCKS * B)
+    for j in range(N):
+        s = compress(dtype, red[j * m:(j + 1) * m], **agp)
+        out += [(j, d, "ag", s) for d in range(N) if d != j]
+    return out

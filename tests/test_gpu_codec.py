@@ -296,3 +296,16 @@ def test_fp8_multichunk_48mib(uz, orc):
         n = (48 << 20) + 123
         bits = synth.normal(n, 0.02, 4, dtype)
         assert gpu_compress(uz, bits, dtype) == orc.compress(dtype, bits)
+
+
+@pytest.mark.parametrize("kind", ["tie", "coded"])
+def test_stored_raw_tie_equals_oracle(uz, orc, kind):
+    """The constructed tie block (roundup16(128 + 2K) == B, stored raw) and the block one 16-byte
+    step below it (coded): GPU stream == oracle stream (tests/test_oracle_rawtie.py pins the oracle)."""
+    from test_oracle_rawtie import tie_input
+    bits = tie_input(kind)
+    ref = orc.compress(BF16, bits)
+    got = gpu_compress(uz, bits, BF16)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, bits.size, BF16)
+    assert st == 0 and np.array_equal(back, bits)

@@ -750,15 +750,9 @@ def test_allreduce_fused_wire_streams_equal_oracle(uz, orc, nr, dtype, codec):
         ref = orc.allreduce(dtype, ins)
         for r in range(nr):
             assert np.array_equal(host(outs[r], dtype), ref), r
-        B = codec.get("block_symbols", 4096)
-        for r in range(nr):
-            for s in range(nr):
-                if s == r:
-                    continue
-                rs = orc.compress(dtype, ins[s][r * m:(r + 1) * m], **codec)
-                assert g.comms[r].read_staging(s, 0, len(rs)) == rs, ("reduce-scatter stream", s, r)
-                ag = orc.compress(dtype, ref[s * m:(s + 1) * m], sample_symbols=8 * B, **codec)
-                assert g.comms[r].read_staging(s, 1, len(ag)) == ag, ("allgather stream", s, r)
+        for s, d, phase, blob in orc.wire_streams("allreduce", dtype, ins, **codec):
+            slot = 0 if phase == "rs" else 1  # the launch uses both slots of every pair
+            assert g.comms[d].read_staging(s, slot, len(blob)) == blob, (phase, s, d)
         st = g.comms[0].stats()
         assert st["compressed"] and st["wire_bytes"] < st["raw_bytes"]
     finally:
@@ -783,5 +777,29 @@ def test_allreduce_fused_many_rounds_and_chunks(uz, orc, dist):
             ref = orc.allreduce(BF16, ins)
             for r in range(nr):
                 assert np.array_equal(host(outs[r], BF16), ref), (it, r)
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("kind", ["allgather", "reduce_scatter"])
+@pytest.mark.parametrize("nr", [2, 3, 4])
+def test_collective_wire_streams_equal_oracle(uz, orc, kind, nr):
+    """Every (src, dst) stream of a compressed allgather / reduce-scatter that lands in dst's
+    staging is the oracle's O13 stream (oracle.wire_streams), byte for byte."""
+    g = Group(uz, nr, staging_bytes=64 << 20, min_compress_bytes=1)
+    try:
+        m = (1 << 20) + 4096 * 9 + 8
+        if kind == "allgather":
+            ins = [synth.weights(m, 61 + r) for r in range(nr)]
+            xs = [dev(b, BF16) for b in ins]
+            outs = [torch.empty(nr * m, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+            g.run(lambda r, c, s: c.all_gather(outs[r], xs[r], s))
+        else:
+            ins = [synth.weights(nr * m, 81 + r) for r in range(nr)]
+            xs = [dev(b, BF16) for b in ins]
+            outs = [torch.empty(m, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+            g.run(lambda r, c, s: c.reduce_scatter(outs[r], xs[r], s))
+        for s, d, _, blob in orc.wire_streams(kind, BF16, ins):
+            assert g.comms[d].read_staging(s, 0, len(blob)) == blob, (s, d)
     finally:
         g.close()
