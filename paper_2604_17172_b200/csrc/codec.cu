@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__
     const uint32_t *dir = reinterpret_cast<const uint32_t *>(in + g.off_dir);
     const unsigned long long *coff = reinterpret_cast<const unsigned long long *>(in + g.off_coff);
     for (uint64_t s0 = cb0; s0 < cb1;) {
-      const uint64_t c = s0 / g.CB;
+      const uint64_t c = chunk_of(g, s0);
       const uint64_t c_first = c * g.CB;
       const uint64_t c_end = min(nb, c_first + g.CB);
       const uint64_t chunk_stop = min(cb1, c_end);

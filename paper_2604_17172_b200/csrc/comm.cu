@@ -196,6 +196,7 @@ void base_plan(uzip_comm *c, Plan &p, int dt) {
   p.ag_job = -1;
   p.dtype = dt;
   p.ticket = ws_ticket(c);
+  p.epoch = reinterpret_cast<uint32_t *>(c->ws + 8);
   p.err = reinterpret_cast<uint32_t *>(c->region);
   p.acc = c->acc;
   p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
@@ -314,12 +315,21 @@ bool needs_coscheduling(const Plan &p) {
 
 uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
   if (c->share > 1 && serialized_env() && needs_coscheduling(p)) return UZIP_ERR_COMM;  // fail fast, no hang
+  plan_flags(p);
   for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
   for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += items_of(p.d[j]);
   p.n_c_items = p.has_copy ? p.c.ntiles : 0;
-  // the sampled tables need no slot: they are built before the credit wait, which they then overlap
+  // the sampled tables: T items at the front of the fused kernel's ticket space (default), or the
+  // k_hist + k_norm launches (A/B), which need no slot and overlap the credit wait
   if (compressed && p.ne > 0) {
-    if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;
+    uint64_t chunks = 0;
+    for (int j = 0; j < p.ne; ++j) chunks = std::max<uint64_t>(chunks, p.e[j].raw ? 0 : p.e[j].g.n_chunks);
+    if (table_kernels(chunks)) {
+      if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;
+      p.tables_ready = 1;
+    } else {
+      for (int j = 0; j < p.ne; ++j) p.n_t_items += t_items_of(p.e[j]);
+    }
   }
   // From the third launch of a call on, a slot's credit comes from a consumer
   // launch of this same call: wait for it in k_credit (one thread) instead of

@@ -46,47 +46,27 @@
 
 namespace uzip {
 
-// ================================================================ k_hist + k_norm
-// a2: k_hist, grid (parts, chunks, streams), 256 threads: part p of chunk c
-// histograms its slice of the chunk's sample ("the first 256 KB") with
-// per-warp shared-memory atomics and stores the partial
-// histogram; it also zeroes the look-back words of the k_fused launch that
-// follows.  a3: k_norm, grid (chunks, streams): sums the partials, applies
-// rule N1 (R5) and writes the chunk's encode entries and 512-byte table.
-// Nothing is accumulated across launches, so nothing needs resetting.
+// ================================================================ a2: sampled histograms
+// Part `part` of chunk c's sample ("the first 256 KB") histogrammed by all 256 threads with
+// per-warp shared-memory atomics into hist (8 x 256 counters, zeroed here); the part's partial
+// histogram is stored to J.partial[c][part].  Used by the T items of k_fused and by k_hist.
 constexpr int kHistThreads = 256;
 constexpr int kHistWarps = kHistThreads / 32;
 
 template <int DT>
-__global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ Plan P) {
-  __shared__ uint32_t hist[kHistWarps][256];
-  const EncJob &J = P.e[blockIdx.z];
-  if (J.raw) return;
+__device__ __forceinline__ void sample_hist(const EncJob &J, uint64_t c, uint32_t part, uint32_t *hist) {
   const StreamGeom &g = J.g;
   const int tid = threadIdx.x, warp = warp_id();
-  const uint32_t part = blockIdx.x, c = blockIdx.y;
-  {  // reset the look-back words of this job for the k_fused launch that follows
-    const uint64_t nctas = (uint64_t)gridDim.x * gridDim.y;
-    const uint64_t me = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
-    for (uint64_t t = me * kHistThreads + tid; t < tiles_of(g); t += nctas * kHistThreads) J.tile_status[t] = 0ull;
-    if (P.ag_job >= 0 && blockIdx.z == 0) {  // ... and those + the table flags of the fused allgather stream
-      const EncJob &A = P.e[P.ag_job];
-      for (uint64_t t = me * kHistThreads + tid; t < tiles_of(A.g); t += nctas * kHistThreads) A.tile_status[t] = 0ull;
-      for (uint64_t c2 = me * kHistThreads + tid; c2 < A.g.n_chunks; c2 += nctas * kHistThreads) A.partial[c2] = 0u;
-    }
-  }
-  if (c >= g.n_chunks) return;
   const uint32_t len = g.sample_len(c), parts = hist_parts(len);
-  if (part >= parts) return;
-  for (int i = tid; i < kHistWarps * 256; i += kHistThreads) (&hist[0][0])[i] = 0;
+  for (int i = tid; i < kHistWarps * 256; i += kHistThreads) hist[i] = 0;
   __syncthreads();
-
   constexpr uint32_t kPer = VecTraits<DT>::kSym;  // symbols per 16-byte vector
   constexpr int kUnroll = 8;
-  const uint8_t *base = J.in + (uint64_t)c * g.CB * g.B * group_bytes(DT);
+  const uint8_t *base = J.in + c * g.CB * g.B * group_bytes(DT);
   const uint32_t nvec = len / kPer;
   const uint32_t per = (nvec + parts - 1) / parts;
   const uint32_t v_lo = part * per, v_hi = min(nvec, v_lo + per);
+  uint32_t *h = hist + 256 * warp;
   for (uint32_t v0 = v_lo; v0 < v_hi; v0 += kHistThreads * kUnroll) {
     uint4 w[kUnroll];
 #pragma unroll
@@ -104,18 +84,30 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
 #pragma unroll
       for (int k = 0; k < (int)kPer; ++k) {
         const uint32_t sy = (sw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-        if (ok) atomicAdd(&hist[warp][sy], 1u);
+        if (ok) atomicAdd(&h[sy], 1u);
       }
     }
   }
   if (part == parts - 1)
     for (uint32_t i = nvec * kPer + tid; i < len; i += kHistThreads)  // sample not a vector multiple
-      atomicAdd(&hist[warp][symbol_at<DT>(base, i)], 1u);
+      atomicAdd(&h[symbol_at<DT>(base, i)], 1u);
   __syncthreads();
   uint32_t sum = 0;
 #pragma unroll
-  for (int w = 0; w < kHistWarps; ++w) sum += hist[w][tid];
-  J.partial[((uint64_t)c * kMaxHistParts + part) * 256 + tid] = sum;
+  for (int w = 0; w < kHistWarps; ++w) sum += hist[256 * w + tid];
+  J.partial[(c * kMaxHistParts + part) * 256 + tid] = sum;
+}
+
+// A/B path (UZIP_TABLE_KERNELS=1): the same table build as two launches ahead of k_fused.
+// k_hist grid (parts, chunks, streams); k_norm grid (chunks, streams) publishes flag = epoch + 1.
+template <int DT>
+__global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ Plan P) {
+  __shared__ uint32_t hist[kHistWarps * 256];
+  const EncJob &J = P.e[blockIdx.z];
+  if (J.raw) return;
+  const uint32_t part = blockIdx.x, c = blockIdx.y;
+  if (c >= J.g.n_chunks || part >= hist_parts(J.g.sample_len(c))) return;
+  sample_hist<DT>(J, c, part, hist);
 }
 
 // a3, all 256 threads of a CTA: thread s holds cnt = count of symbol s in the chunk's sample; rule
@@ -186,12 +178,24 @@ __global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
   uint32_t sum = 0;
   for (uint32_t p = 0; p < parts; ++p) sum += J.partial[((uint64_t)c * kMaxHistParts + p) * 256 + tid];
   norm_tables(sum, J.enc + c * 256, J.tab16 + c * 256, nullptr, red64, red32);
+  if (tid == 0) {
+    __threadfence();
+    st_release_gpu_u32(J.tflag + c, (*P.epoch & kEpochMask) + 1u);
+  }
 }
 
 // ================================================================ shared pieces
+// Look-back word: flag (2 bits: 1 aggregate, 2 inclusive prefix) | launch epoch (24 bits) | value
+// (38 bits: stream offsets < 256 GiB).  A word whose epoch is not this launch's is "not ready", so
+// the words never need resetting between launches (a 2^24-launch wrap could only alias a tile word
+// left untouched for exactly that many launches of the same workspace).
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagInc = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
+constexpr int kEpochShift = 38;
+constexpr unsigned long long kValMask = (1ull << kEpochShift) - 1;
+__device__ __forceinline__ unsigned long long ep_bits(uint32_t ep) {
+  return (unsigned long long)(ep & kEpochMask) << kEpochShift;
+}
 
 __device__ __forceinline__ void raise_err(const Plan &P, uint32_t code) { atomicCAS(P.err, 0u, code); }
 // First error only: the code plus where it happened (site, expected, seen) for uzip_comm_error_detail.
@@ -280,20 +284,22 @@ static __device__ bool wait_u32(const Plan &P, const uint32_t *f, uint32_t want,
 // aggregate can be published as soon as a tile is coded and the scan finished
 // later.  publish: one thread.  finish: one full warp; returns the exclusive
 // prefix of tile t, or ~0 on abort.
-__device__ __forceinline__ void lookback_publish(unsigned long long *status, uint64_t t, unsigned long long agg) {
-  st_relaxed_u64(&status[t], (t == 0 ? kFlagInc : kFlagAgg) | agg);
+__device__ __forceinline__ void lookback_publish(unsigned long long *status, uint64_t t, unsigned long long agg,
+                                                 uint32_t ep) {
+  st_relaxed_u64(&status[t], (t == 0 ? kFlagInc : kFlagAgg) | ep_bits(ep) | agg);
 }
 
 static __device__ unsigned long long lookback_finish(const Plan &P, unsigned long long *status, uint64_t t,
-                                              unsigned long long agg) {
+                                              unsigned long long agg, uint32_t ep) {
   const int lane = threadIdx.x & 31;
   if (t == 0) return 0;
   unsigned long long excl = 0, t0 = 0;
   int64_t base = (int64_t)t - 1;
+  const unsigned long long eb = ep_bits(ep), emask = (unsigned long long)kEpochMask << kEpochShift;
   for (int spin = 0;; ++spin) {
     const int64_t idx = base - lane;
-    unsigned long long s = idx >= 0 ? ld_relaxed_u64(&status[idx]) : (kFlagInc | 0ull);
-    const uint32_t flag = (uint32_t)(s >> 62);
+    unsigned long long s = idx >= 0 ? ld_relaxed_u64(&status[idx]) : (kFlagInc | eb);
+    const uint32_t flag = (s & emask) == eb ? (uint32_t)(s >> 62) : 0u;  // another launch's word: not ready
     const uint32_t inc = __ballot_sync(0xFFFFFFFFu, flag == 2);
     const uint32_t notready = __ballot_sync(0xFFFFFFFFu, flag == 0);
     const int first_inc = inc ? __ffs(inc) - 1 : 31;
@@ -319,14 +325,14 @@ static __device__ unsigned long long lookback_finish(const Plan &P, unsigned lon
     if (inc) break;
     base -= 32;
   }
-  if (lane == 0) st_relaxed_u64(&status[t], kFlagInc | (excl + agg));
+  if (lane == 0) st_relaxed_u64(&status[t], kFlagInc | eb | (excl + agg));
   return excl;
 }
 
 static __device__ unsigned long long lookback(const Plan &P, unsigned long long *status, uint64_t t,
-                                       unsigned long long agg) {
-  if ((threadIdx.x & 31) == 0) lookback_publish(status, t, agg);
-  return lookback_finish(P, status, t, agg);
+                                       unsigned long long agg, uint32_t ep) {
+  if ((threadIdx.x & 31) == 0) lookback_publish(status, t, agg, ep);
+  return lookback_finish(P, status, t, agg, ep);
 }
 
 // ---------------------------------------------------------------- fp32 fold helpers (a9, R11)
@@ -414,6 +420,8 @@ struct FusedShared {
   unsigned long long src_payload[kMaxRanks];
   uint32_t red[kWarps];
   unsigned long long red64[kWarps];
+  uint32_t epoch;  // this launch's epoch (Plan::epoch)
+  uint32_t is_last;
 };
 
 // ---------------------------------------------------------------- E item
@@ -648,14 +656,14 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
   const uint64_t t = pd.t;
   pd.job = -1;
   if (warp == 0) {
-    const unsigned long long excl = lookback_finish(P, J.tile_status, t, S.pagg);
+    const unsigned long long excl = lookback_finish(P, J.tile_status, t, S.pagg, S.epoch);
     if (lane == 0) S.ptile_off = excl;
   }
   __syncthreads();
   const unsigned long long tile_off = S.ptile_off;
   if (tile_off != ~0ull) {
     const uint64_t b0 = t * kTileBlocks, b = b0 + warp;
-    const uint64_t c = b0 / g.CB;
+    const uint64_t c = chunk_of(g, b0);
     uint32_t roff = 0;
     for (int w = 0; w < warp; ++w) roff += S.psize[w];
     const uint32_t size = S.psize[warp];
@@ -664,19 +672,18 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
       for (uint32_t d = 0; d < J.nd; ++d) {
         if (lane == 0) {
           reinterpret_cast<uint32_t *>(J.dst[d] + g.off_dir)[b] = S.pkdir[warp];
-          if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[b / g.CB] = off;
+          if ((uint32_t)b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[chunk_of(g, b)] = off;
         }
         uint4 *o = reinterpret_cast<uint4 *>(J.dst[d] + g.off_pay + off);
         for (uint32_t i = lane; i < size / 16; i += 32) o[i] = reinterpret_cast<const uint4 *>(ring + roff)[i];
       }
       if (b == g.n_blocks - 1) finalize_stream<DT>(J, off + size);
     }
-    if (b0 % g.CB == 0 && warp == kWarps - 1) {  // the chunk's first tile carries its table
+    if ((uint32_t)b0 % g.CB == 0 && warp == kWarps - 1) {  // the chunk's first tile carries its table
       const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
       for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
     }
-    bool flags = false;
-    for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+    const bool flags = J.has_flags != 0;
     if (flags) {
       __syncwarp();
       if (lane == 0) {
@@ -696,6 +703,42 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
     }
   }
   __syncthreads();  // the ring and the pending sizes are free again
+}
+
+// T item (a2 + a3 inside the fused kernel): part `part` of chunk c's sample is
+// histogrammed into J.partial; the last part of the chunk to finish (epoch-tagged counter, so
+// nothing is reset between launches) sums the partials, applies rule N1 and publishes the chunk's
+// encode entries, serialized table and flag = epoch + 1.  E items of the chunk wait for the flag.
+template <int DT, int B>
+static __device__ void t_item(const Plan &P, const EncJob &J, uint64_t c, uint32_t part, uint8_t *smem,
+                              FusedShared &S) {
+  using C = FusedCfg<DT, B>;
+  const int tid = threadIdx.x;
+  uint32_t *hist = reinterpret_cast<uint32_t *>(smem + C::kEncTab);  // the warp buffers (free between items)
+  sample_hist<DT>(J, c, part, hist);
+  const uint32_t parts = hist_parts(J.g.sample_len(c)), ep = S.epoch;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();  // the partial is visible before it is counted
+    uint32_t old = ld_volatile_u32(J.tcount + c), want;
+    for (;;) {
+      want = (old >> 8) == ep ? old + 1u : ((ep << 8) | 1u);  // first part of this launch restarts the count
+      const uint32_t seen = atomicCAS(J.tcount + c, old, want);
+      if (seen == old) break;
+      old = seen;
+    }
+    S.is_last = (want & 0xFFu) == parts ? 1u : 0u;
+    __threadfence();
+  }
+  __syncthreads();
+  if (!S.is_last) return;
+  uint32_t sum = 0;
+  for (uint32_t p = 0; p < parts; ++p) sum += ld_cg_u32(J.partial + (c * kMaxHistParts + p) * 256 + tid);
+  norm_tables(sum, J.enc + c * 256, J.tab16 + c * 256, nullptr, S.red64, S.red);
+  if (tid == 0) {
+    __threadfence();
+    st_release_gpu_u32(J.tflag + c, ep + 1u);
+  }
 }
 
 // The destinations' slots of encode job jidx are free (a12): the first tile of the job in this CTA
@@ -724,14 +767,13 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
                                  FusedShared &S, uint8_t *ring, int ring_bytes, EncPending &pd, const uint8_t *in) {
   using C = FusedCfg<DT, B>;
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  bool flags = false;
-  for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+  const bool flags = J.has_flags != 0;
   const StreamGeom &g = J.g;
   const uint4 *tab = reinterpret_cast<const uint4 *>(smem);
   uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
   uint16_t *buf16 = reinterpret_cast<uint16_t *>(buf);
   const uint64_t b0 = t * kTileBlocks;
-  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t c = g.n_blocks ? chunk_of(g, b0) : 0;
   const uint64_t b = b0 + warp;
   const uint8_t *src = in + b * (uint64_t)B * group_bytes(DT);
   uint32_t size = 0, kdir = 0, K = 0, x = kL;
@@ -783,14 +825,14 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
     }
     if (tid == 0) {
       S.pagg = sum;
-      lookback_publish(J.tile_status, t, sum);
+      lookback_publish(J.tile_status, t, sum, S.epoch);
     }
     pd.job = jidx;
     pd.t = t;
     return;  // the item-end barrier publishes the ring contents to the resolving warps
   }
   if (warp == 0) {
-    const unsigned long long excl = lookback(P, J.tile_status, t, sum);
+    const unsigned long long excl = lookback(P, J.tile_status, t, sum, S.epoch);
     if (lane == 0) S.tile_off = excl;
   }
   __syncthreads();
@@ -804,7 +846,7 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
       uint8_t *o = J.dst[d] + g.off_pay + off;
       if (lane == 0) {
         reinterpret_cast<uint32_t *>(J.dst[d] + g.off_dir)[b] = kdir;
-        if (b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[b / g.CB] = off;
+        if ((uint32_t)b % g.CB == 0) reinterpret_cast<unsigned long long *>(J.dst[d] + g.off_coff)[chunk_of(g, b)] = off;
       }
       if (raw) {
         for (uint32_t i = lane; i < size / 16; i += 32)
@@ -834,7 +876,7 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
     finalize_stream<DT>(J, 0ull);
   }
   // the chunk's first tile carries its serialized table (the receiver waits for it)
-  if (g.n_blocks && b0 % g.CB == 0 && warp == kWarps - 1) {
+  if (g.n_blocks && (uint32_t)b0 % g.CB == 0 && warp == kWarps - 1) {
     const uint4 v = reinterpret_cast<const uint4 *>(J.tab16 + c * 256)[lane];
     for (uint32_t d = 0; d < J.nd; ++d) reinterpret_cast<uint4 *>(J.dst[d] + g.off_tab + 512ull * c)[lane] = v;
   }
@@ -866,8 +908,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   const int tid = threadIdx.x, warp = warp_id();
   (void)next_it;  // an L2 prefetch of the next tile by warp 0 was measured slower (r1: 0.784 vs 0.754 ms/GiB)
   if (!credit_gate(P, J, jidx, credit_done, S)) return;
-  bool flags = false;
-  for (uint32_t d = 0; d < J.nd; ++d) flags |= J.flag[d] != nullptr;
+  const bool flags = J.has_flags != 0;
 
   if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
     const uint64_t o0 = t * kRawTileBytes;
@@ -899,10 +940,18 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   // first); the coded words grow from byte 0 into the rows already consumed.
   uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
   const uint64_t b0 = t * kTileBlocks;
-  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t c = g.n_blocks ? chunk_of(g, b0) : 0;
   const uint64_t key = ((uint64_t)jidx << 48) | c;
   if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
-    tab[tid] = J.enc[c * 256 + tid];
+    if (!P.tables_ready) {
+      if (tid == 0) {  // the chunk's table: published by its last T item (a smaller ticket)
+        unsigned long long seen = 0;
+        S.abort = wait_u32(P, J.tflag + c, S.epoch + 1u, seen) ? 0u : 1u;
+      }
+      __syncthreads();
+      if (S.abort) return;
+    }
+    tab[tid] = J.enc[c * 256 + tid];  // after the acquire (gpu scope): plain loads see the T item's stores
     enc_key = key;
     __syncthreads();
   }
@@ -947,7 +996,7 @@ static __device__ void acquire_tile(const Plan &P, const DecJob &J, uint32_t s, 
   bool ok = wait_flag(P, J.flag[s] + t, J.epoch[s], v);
   S.src_off[s] = (v & 0xFFFFFFFFull) << 4;
   if (ok && need_table && !J.raw && J.g.n_blocks) {
-    const uint64_t first = (t * kTileBlocks / J.g.CB) * J.g.CB / kTileBlocks;
+    const uint64_t first = (uint64_t)chunk_of(J.g, t * kTileBlocks) * J.g.CB / kTileBlocks;
     if (first != t) {
       unsigned long long v2;
       ok = wait_flag(P, J.flag[s] + first, J.epoch[s], v2);
@@ -1043,8 +1092,8 @@ static __device__ void forward_tile(const Plan &P, const DecJob &J, uint64_t t, 
     }
     fwd_range(J, stream, g.off_dir + 4 * b0, 4 * nblk);
     fwd_range(J, stream, g.off_pay + tile_off, tile_end - tile_off);
-    if (b0 % g.CB == 0) {
-      const uint64_t c = b0 / g.CB;
+    if ((uint32_t)b0 % g.CB == 0) {
+      const uint64_t c = chunk_of(g, b0);
       fwd_range(J, stream, g.off_tab + 512 * c, 512);
       fwd_range(J, stream, g.off_coff + 8 * c, 8);
     }
@@ -1071,7 +1120,7 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
   const int tid = threadIdx.x, warp = warp_id();
   const StreamGeom &g = J.g;
   const uint64_t b0 = t * kTileBlocks;
-  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t c = g.n_blocks ? chunk_of(g, b0) : 0;
   const uint64_t key = (1ull << 63) | ((uint64_t)jidx << 48) | c;
   const bool need_table = key != dec_key;
   if (tid == 0) acquire_tile(P, J, 0, t, need_table, S);
@@ -1212,7 +1261,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
   }
 
   const uint64_t b0 = t * kTileBlocks;
-  const uint64_t c = g.n_blocks ? b0 / g.CB : 0;
+  const uint64_t c = g.n_blocks ? chunk_of(g, b0) : 0;
   const uint64_t b = b0 + warp;
   uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + C::ring(true));
   float *acc = P.acc + ((uint64_t)blockIdx.x * kWarps + warp) * B;
@@ -1330,11 +1379,11 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
   if (ag) {
     const EncJob &A = P.e[P.ag_job];
     const StreamGeom &ga = A.g;
-    const uint64_t ca = ga.n_blocks ? b0 / ga.CB : 0;
+    const uint64_t ca = ga.n_blocks ? chunk_of(ga, b0) : 0;
     const uint64_t key = ((uint64_t)P.ag_job << 48) | ca;
     uint4 *tab = reinterpret_cast<uint4 *>(smem);
-    uint32_t *tabflag = A.partial;  // per chunk: 1 = table published (reset by k_hist)
-    if (ga.n_blocks && b0 % ga.CB == 0) {
+    uint32_t *tabflag = A.tflag;  // per chunk: epoch + 1 = table published
+    if (ga.n_blocks && (uint32_t)b0 % ga.CB == 0) {
       // the chunk's first tile is its sample (R26): histogram the symbols just split, rule N1, publish
       uint32_t *hist = dtab;  // 8 x 256 counters in the decode-table region
       dec_key = ~0ull;
@@ -1355,13 +1404,13 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
       norm_tables(cnt, A.enc + ca * 256, A.tab16 + ca * 256, tab, S.red64, S.red);
       if (tid == 0) {
         __threadfence();
-        st_release_gpu_u32(tabflag + ca, 1u);
+        st_release_gpu_u32(tabflag + ca, S.epoch + 1u);
       }
       enc_key = key;
     } else if (ga.n_blocks && key != enc_key) {
       if (tid == 0) {  // the chunk's first tile (a smaller ticket) publishes the table
         unsigned long long v = 0;
-        S.abort = wait_u32(P, tabflag + ca, 1u, v) ? 0u : 1u;
+        S.abort = wait_u32(P, tabflag + ca, S.epoch + 1u, v) ? 0u : 1u;
       }
       __syncthreads();
       if (S.abort) return;
@@ -1389,9 +1438,10 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
   using Cf = FusedCfg<DT, B>;
   uint8_t *ring = smem + Cf::kEncTab + kWarps * Cf::kWarpBuf;
   EncPending pd{-1, 0};
-  const uint64_t ne = P.n_e_items, nc = P.n_c_items, total = ne + nc + P.n_d_items;
+  const uint64_t nt = P.n_t_items, ne = P.n_e_items, nc = P.n_c_items, total = nt + ne + nc + P.n_d_items;
   if (tid == 0) {
     S.tile_cnt = 0;
+    S.epoch = ld_volatile_u32(P.epoch) & kEpochMask;  // advanced only after every CTA has left
     S.tk[0] = atomicAdd(P.ticket, 1u);
   }
   __syncthreads();
@@ -1420,7 +1470,16 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
       // decode-only launch (P2P / broadcast receivers): no E/C item code in this instantiation, so
       // its register budget is the decoder's alone
       decode_items(it);
+    } else if (it < nt) {  // T items: job-major, then chunk, then part (no pending tile exists yet)
+      uint64_t k = it;
+      int j = 0;
+      while (j + 1 < P.ne && k >= t_items_of(P.e[j])) k -= t_items_of(P.e[j++]);
+      uint64_t c;
+      uint32_t part;
+      t_item_at(P.e[j], k, c, part);
+      t_item<DT, B>(P, P.e[j], c, part, smem, S);
     } else {
+      it -= nt;
       const bool coded_e = it < ne && !P.e[it % (uint64_t)P.ne].raw;
       if (pd.job >= 0 && !coded_e) resolve_pending<DT, B>(P, S, ring, pd);
       if (it < ne) {
@@ -1443,6 +1502,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
     if (atomicAdd(P.ticket + 1, 1u) == gridDim.x - 1) {
       P.ticket[0] = 0;
       P.ticket[1] = 0;
+      *P.epoch = (S.epoch + 1u) & kEpochMask;  // every CTA read it at its start
       if (P.codec_call) {  // uzip_compress: the error word is private to this call
         if (ld_volatile_u32(P.err))
           for (int j = 0; j < P.ne; ++j)
@@ -1508,7 +1568,7 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
   if (occ <= 0) occ = 1;
-  const uint64_t items = p.n_e_items + p.n_c_items + p.n_d_items;
+  const uint64_t items = p.n_t_items + p.n_e_items + p.n_c_items + p.n_d_items;
   int grid = sm_count() * occ;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   // Ranks sharing this GPU (loopback): a launch whose decode items spin on a

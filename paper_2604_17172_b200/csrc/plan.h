@@ -21,6 +21,7 @@
 namespace uzip {
 
 constexpr int kMaxRanks = 8;
+constexpr uint32_t kEpochMask = (1u << 24) - 1;  // launch epochs (Plan::epoch) are 24-bit
 constexpr uint32_t kRawTileBytes = 64u << 10;
 
 // Tiles (kTileBlocks blocks each) of a stream; a stream without whole blocks
@@ -30,6 +31,9 @@ __host__ __device__ inline uint64_t tiles_of(const StreamGeom &g) {
   return t ? t : 1;
 }
 
+// Tables of an encode job are built inside the fused kernel by T items (a2 + a3): one per part of
+// each chunk's sample; the last part of a chunk to finish applies rule N1 and publishes the chunk's
+// table flag = epoch + 1 (table build fused into the single kernel).
 struct EncJob {
   const uint8_t *in;                        // local input of this stream
   StreamGeom g;                             // geometry (compressed mode)
@@ -37,6 +41,7 @@ struct EncJob {
   uint64_t ntiles;                          // >= 1
   uint32_t raw;                             // 1 = raw (uncoded) tiles
   uint32_t nd;                              // destinations
+  uint32_t has_flags;                       // some destination has tile flags (set by plan_flags)
   uint8_t *dst[kMaxRanks];                  // stream base at each destination
   unsigned long long *flag[kMaxRanks];      // tile flags at each destination (null: no flags)
   const unsigned long long *credit[kMaxRanks];  // local word: last epoch the destination consumed from this slot
@@ -44,7 +49,9 @@ struct EncJob {
   uint4 *enc;                               // per-chunk encode entries (k_norm)
   uint16_t *tab16;                          // per-chunk serialized tables (k_norm)
   unsigned long long *tile_status;          // per-tile look-back words (zeroed by k_hist)
-  uint32_t *partial;                        // k_hist partial histograms [chunk][kMaxHistParts][256]
+  uint32_t *partial;                        // partial histograms [chunk][kMaxHistParts][256]
+  uint32_t *tflag;                          // per chunk: table published = epoch + 1
+  uint32_t *tcount;                         // per chunk: (epoch << 8) | parts done (T items)
   uint64_t *d_out_bytes;                    // codec: stream size (may be null)
   unsigned long long *wire_acc;             // comm: += stream bytes x nd (may be null)
 };
@@ -91,8 +98,11 @@ struct Plan {
   EncJob e[kMaxRanks];
   DecJob d[kMaxRanks];
   CopyJob c;
-  uint64_t n_e_items, n_c_items, n_d_items;
+  uint64_t n_t_items, n_e_items, n_c_items, n_d_items;
   uint32_t *ticket;                         // self-resetting ticket + exit counter (2 words)
+  uint32_t *epoch;                          // launch epoch of this workspace (24 bits): read by every CTA at
+                                            // start, advanced by the last CTA out; tags the look-back words
+                                            // and the per-chunk table flags, so nothing needs resetting
   uint32_t *err;                            // sticky async error word
   uint64_t timeout_ns;
   int32_t ring_bytes;                       // set by the launcher: smem ring for parked coded tiles
@@ -107,6 +117,8 @@ struct Plan {
   // code it straight into that stream (one pass, no HBM round trip); the chunk's first tile samples
   // the table (tabflag[c] = e[ag_job].partial[c] publishes it to the other tiles of the chunk).
   int32_t ag_job;                           // -1: none
+  uint32_t tables_ready;                    // 1: k_hist + k_norm built every encode table before this
+                                            // launch (stream order), E items skip the table flag wait
 };
 
 // Slot credits one launch needs (a12), waited for by k_credit -- one thread --
@@ -135,7 +147,7 @@ __host__ __device__ inline uint32_t hist_parts(uint32_t sample_len) {
 struct EncWs {
   static uint64_t bytes(uint64_t n_chunks, uint64_t n_blocks) {
     return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * (n_blocks + 1)) +
-           round16(1024ull * kMaxHistParts * n_chunks);
+           round16(1024ull * kMaxHistParts * n_chunks) + 2 * round16(4 * n_chunks);
   }
   static void carve(uint8_t *p, uint64_t n_chunks, uint64_t n_blocks, EncJob &j) {
     j.enc = reinterpret_cast<uint4 *>(p);
@@ -145,8 +157,38 @@ struct EncWs {
     j.tile_status = reinterpret_cast<unsigned long long *>(p);
     p += round16(8 * (n_blocks + 1));
     j.partial = reinterpret_cast<uint32_t *>(p);
+    p += round16(1024ull * kMaxHistParts * n_chunks);
+    j.tflag = reinterpret_cast<uint32_t *>(p);
+    p += round16(4 * n_chunks);
+    j.tcount = reinterpret_cast<uint32_t *>(p);
   }
 };
+
+// T items of an encode job: every chunk's sample split into hist_parts(sample) parts (all chunks but
+// the last have the same sample length).
+__host__ __device__ inline uint64_t t_items_of(const EncJob &J) {
+  if (J.raw || J.g.n_blocks == 0) return 0;
+  const uint64_t nc = J.g.n_chunks;
+  return (nc - 1) * hist_parts(J.g.sample_len(0)) + hist_parts(J.g.sample_len(nc - 1));
+}
+__host__ __device__ inline void t_item_at(const EncJob &J, uint64_t k, uint64_t &c, uint32_t &part) {
+  const uint64_t nc = J.g.n_chunks, pf = hist_parts(J.g.sample_len(0));
+  if (k < (nc - 1) * pf) {
+    c = k / pf;
+    part = (uint32_t)(k % pf);
+  } else {
+    c = nc - 1;
+    part = (uint32_t)(k - (nc - 1) * pf);
+  }
+}
+
+// Host: derive EncJob::has_flags of every encode job of a plan (call before the launch).
+inline void plan_flags(Plan &p) {
+  for (int j = 0; j < kMaxRanks; ++j) {
+    p.e[j].has_flags = 0;
+    for (uint32_t d = 0; d < p.e[j].nd; ++d) p.e[j].has_flags |= p.e[j].flag[d] != nullptr;
+  }
+}
 
 static_assert(sizeof(Plan) <= 30000, "kernel parameter space");
 

@@ -43,6 +43,7 @@ __host__ __device__ constexpr uint64_t round16(uint64_t v) { return (v + 15u) & 
 struct StreamGeom {
   uint64_t n, n_blocks, n_coded, n_chunks;
   uint32_t B, CB, S, global, dtype, eb;
+  uint32_t cb_log2;                       // log2(CB) if CB is a power of 2 (> 1), else 0
   uint64_t off_res0, off_res1, off_tab, off_coff, off_dir, off_pay;
 
   __host__ __device__ void init(int dt, uint64_t n_, uint32_t B_, uint32_t CB_, uint32_t S_, bool global_) {
@@ -61,6 +62,9 @@ struct StreamGeom {
       S = S_;
     }
     n_chunks = (n_blocks + CB - 1) / CB;
+    cb_log2 = 0;
+    if (CB > 1 && (CB & (CB - 1)) == 0)
+      while ((1u << cb_log2) < CB) ++cb_log2;
     off_res0 = kHeaderBytes;
     if (dt == kF32) {
       off_res1 = off_res0 + 2 * n_coded;
@@ -87,6 +91,12 @@ struct StreamGeom {
     return (uint32_t)((S == 0 || S > syms) ? syms : S);
   }
 };
+
+// Chunk of block b: 32-bit division (block indices fit 32 bits: the directory is u32), which
+// compiles inline instead of the 64-bit division's runtime call.
+__host__ __device__ __forceinline__ uint32_t chunk_of(const StreamGeom &g, uint64_t b) {
+  return g.cb_log2 ? (uint32_t)b >> g.cb_log2 : (uint32_t)b / g.CB;  // default CB (1024 / 512) is a power of 2
+}
 
 // Decoder control words at the start of the caller's workspace (uzip_decompress): the first error
 // and the CTA arrival counter, both reset by the last CTA (the encoder's workspace is EncWs, plan.h).

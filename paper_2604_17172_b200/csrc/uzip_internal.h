@@ -14,4 +14,9 @@ cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void
 // UZIP_OK or UZIP_ERR_INVALID_ARG for unsupported values.
 uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g);
 
+// Whether a launch whose largest encode stream has n_chunks table chunks builds its tables with
+// the k_hist + k_norm launches (true) or with T items inside k_fused (false); UZIP_TABLE_KERNELS
+// overrides (A/B of the single-kernel table build).
+bool table_kernels(uint64_t n_chunks);
+
 }  // namespace uzip

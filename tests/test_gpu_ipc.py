@@ -80,3 +80,16 @@ def test_serialized_execution_fails_fast(env):
                        timeout=300, cwd=ROOT, env=dict(os.environ, **env))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "smoke ok" in r.stdout and "serialized ok" in r.stdout
+
+
+def test_table_kernel_path_equals_oracle():
+    """The A/B table build (UZIP_TABLE_KERNELS=1: k_hist + k_norm launched ahead of k_fused instead
+    of the T items inside it) produces the same oracle streams on the codec and the collectives."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, UZIP_TABLE_KERNELS="1")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_codec.py"), os.path.join(ROOT, "tests", "test_gpu_comm.py"), "-k",
+           "stream_bytes_equal_oracle or stream_params or wire_stream or allreduce_fused or tie"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
