@@ -293,7 +293,7 @@ cudaError_t launch_decode_t(const void *in, uint64_t in_bytes, void *out, uint64
   }
   int grid = sm_count() * occupancy(kern, 256, DecShared::kBytes);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  const uint64_t want = (est_blocks + 3) / 4;
+  const uint64_t want = (est_blocks + kWarps - 1) / kWarps;  // >= one block per warp: one table build per 8 blocks
   if ((uint64_t)grid > want) grid = (int)(want ? want : 1);
   kern<<<grid, 256, DecShared::kBytes, st>>>((const uint8_t *)in, in_bytes, (uint8_t *)out, n, ws, d_status);
   return cudaGetLastError();
@@ -302,7 +302,9 @@ cudaError_t launch_decode_t(const void *in, uint64_t in_bytes, void *out, uint64
 
 cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void *out, uint64_t n, void *ws,
                               int32_t *d_status, cudaStream_t st, int max_ctas) {
-  const uint64_t est_blocks = n / 1024;
+  // the block size is in the (device-side) header; size the grid for the default B = 4096 (a
+  // B = 1024 stream then gets 4 blocks per warp, still plenty of CTAs once it is large)
+  const uint64_t est_blocks = n / 4096;
   switch (dtype) {
     case kBF16: return launch_decode_t<kBF16>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
     case kF16: return launch_decode_t<kF16>(in, in_bytes, out, n, ws, d_status, st, max_ctas, est_blocks);
