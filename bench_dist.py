@@ -222,11 +222,22 @@ def run(args):
             in_stream(lambda: dist.broadcast(wb, 0)), 2 * n)
     assert comm.async_error() == 0
 
+    # ---- BASELINE configs[1..4] sweeps, each bounded in time; results keyed by config
+    suites = run_suites(args, uz, comm, stream, rank, world, local, x, y, role, peer, n)
+
     sts = [None] * world
     dist.all_gather_object(sts, st)
     if rank == 0:
         ratio = next((s["wire_bytes"] / s["raw_bytes"] for s in sts if s), None)
         wire_gbs = (ratio or 1.0) * 2 * n / (ms / 1e3) / GB
+        hbm, _ = bench.peaks()
+        r = ratio or 1.0
+        S = 2 * n
+        # transfer roofline (north_star): the slower of codec-at-HBM-peak (receiver: r*S written by the
+        # sender + r*S read + S written; sender: S read) and the compressed bytes over one NVLink direction
+        t_codec = max(S, (2 * r + 1) * S) / (hbm * GB)
+        t_wire = r * S / (770.0 * GB)
+        t_bound = max(t_codec, t_wire)
         line = {
             "metric": "effective uncompressed GB/s", "value": round(raw / (ms / 1e3) / GB, 3), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -236,16 +247,231 @@ def run(args):
                                "ms_per_step": round(ms_nccl, 4)},
             "collectives": coll,
             "ablation": ablation,
-            "roofline": {"bound": "nvlink", "kernel": "k_fused (sender: encode + P2P stores)",
+            "roofline": {"bound": "nvlink", "kernel": "k_fused (sender E items + receiver D items, split-send)",
                          "achieved": round(wire_gbs, 1), "peak": 770.0, "unit": "GB/s",
                          "peak_source": "B200_PROFILING.md measured peer copy per direction",
-                         "frac": round(wire_gbs / 770.0, 4), "traffic": None},
+                         "frac": round(wire_gbs / 770.0, 4), "traffic": None,
+                         "transfer_bound_ms": round(t_bound * 1e3, 4),
+                         "transfer_frac": round(t_bound / (ms / 1e3 / max(1, pairs)) if pairs else 0.0, 4),
+                         "note": "transfer_frac = max(codec at HBM peak, r*S / 770 GB/s) / time per pair"},
             "e2e": {"value": round(raw / e2e_s / GB, 3), "unit": "GB/s", "h2d_bytes_per_step": pairs * 2 * n,
                     "d2h_bytes_per_step": pairs * 16, "ms_per_step": round(e2e_s * 1e3, 3)},
             "clocks": clk.summary(),
             "gpu_launches": args.steps * 2 * 2 * max(1, (2 * n) // (256 << 20)),
+            "versions": versions(),
+            "suites": suites,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
+
+
+def versions():
+    import subprocess
+    v = {"torch": torch.__version__, "cuda": torch.version.cuda}
+    try:
+        nv = torch.cuda.nccl.version()
+        v["nccl"] = ".".join(map(str, nv)) if isinstance(nv, tuple) else str(nv)
+    except Exception as e:  # pragma: no cover
+        v["nccl"] = repr(e)[:80]
+    try:
+        v["driver"] = subprocess.run(["nvidia-smi", "--query-gpu=driver_version,name", "--format=csv,noheader"],
+                                     capture_output=True, text=True, timeout=20).stdout.splitlines()[0].strip()
+    except Exception as e:  # pragma: no cover
+        v["driver"] = repr(e)[:80]
+    v["NCCL_ALGO"] = os.environ.get("NCCL_ALGO", "default")
+    return v
+
+
+def _fill_w(buf, seed):
+    """W = bf16(N(0, 0.02)) in 64 Mi-element slices (no fp32 temporary of the whole buffer)."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    flat = buf.view(-1)
+    step = 64 << 20
+    for o in range(0, flat.numel(), step):
+        k = min(step, flat.numel() - o)
+        flat[o:o + k].copy_(torch.randn(k, device="cuda", generator=g) * 0.02)
+    return buf
+
+
+def run_suites(args, uz, comm, stream, rank, world, local, x, y, role, peer, n):
+    """BASELINE configs[1]-[4] as sweeps: C2 pipe-chunk x block-size grid, C3 Qwen2.5-7B
+    weight sync (per tensor and 256 MiB buckets) vs NCCL broadcast, C4 activation allreduce
+    256 KiB-256 MiB vs NCCL, C5 allgather / reduce-scatter 1 MiB-4 GiB vs NCCL, KV-cache P2P.
+    Every entry: uzip and NCCL algbw (GB/s, nccl-tests convention) and the wire ratio.  Each suite
+    is skipped once the budget (UZIP_BENCH_BUDGET_S, default 900 s) is spent; UZIP_BENCH_SUITES
+    selects a comma-separated subset ("none" skips all)."""
+    budget = float(os.environ.get("UZIP_BENCH_BUDGET_S", "900"))
+    want = os.environ.get("UZIP_BENCH_SUITES", "c2_grid,c4_allreduce,c5_ag_rs,kv_p2p,c3_weight_sync")
+    t0 = time.time()
+    out = {}
+    steps = max(1, min(args.steps, 2 if SMOKE else 5))
+    warm = 1
+    MB = 1 << 20
+
+    def timed(fn):
+        return _timed(fn, stream, steps, warm)
+
+    def gbs(nbytes, ms_):
+        return round(nbytes / (ms_ / 1e3) / GB, 2) if ms_ == ms_ and ms_ > 0 else None
+
+    def in_stream(f):
+        def g():
+            with torch.cuda.stream(stream):
+                f()
+        return g
+
+    def pair(uz_fn, nccl_fn, user_bytes, cm=None):
+        cm = cm or comm
+        mu = timed(in_stream(uz_fn))
+        stt = cm.stats()
+        mn = float("nan") if SMOKE or nccl_fn is None else timed(in_stream(nccl_fn))
+        return {"uzip_GBps": gbs(user_bytes, mu), "nccl_GBps": gbs(user_bytes, mn), "ms": round(mu, 4),
+                "ms_nccl": round(mn, 4) if mn == mn else None,
+                "wire_ratio": round(stt["wire_bytes"] / max(1, stt["raw_bytes"]), 5)}
+
+    def suite(name, fn):
+        if name not in want.split(","):
+            return
+        if time.time() - t0 > budget:
+            out[name] = {"skipped": f"time budget {budget:.0f} s spent"}
+            return
+        ts = time.time()
+        out[name] = fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        out[name]["seconds"] = round(time.time() - ts, 1)
+
+    pairs = world // 2
+
+    def c2_grid():
+        """split-send P2P of the 1 GiB shard, pairs (2i -> 2i+1): pipe chunk x codec block size."""
+        res = {}
+        chunks = (4, 64) if SMOKE else (4, 16, 64, 256, 1024)
+        for B in (1024, 2048, 4096):
+            for pc in chunks:
+                stg = max(512 * MB, 2 * pc * MB)
+                cm = uz.Comm.from_group(None, local, block_symbols=B, pipe_chunk_bytes=pc * MB,
+                                        staging_bytes=min(stg, 32 * MB) if SMOKE else stg,
+                                        **(dict(max_ctas=16, poll_timeout_ms=60000) if SMOKE else {}))
+
+                def step():
+                    if role == "send":
+                        cm.send(x, peer, stream)
+                    elif role == "recv":
+                        cm.recv(y, peer, stream)
+                ms_ = timed(in_stream(step))
+                assert cm.async_error() == 0
+                res[f"B{B}_chunk{pc}MiB"] = gbs(pairs * 2 * n, ms_)
+                cm.destroy()
+        res["note"] = "GB/s of all pairs; B in {8192, 16384} unsupported (kMaxB = 4096, smem staging)"
+        return res
+
+    def c4_allreduce():
+        """Llama-3-8B TP activation allreduce, T = 32 * 2^k tokens x 4096 (256 KiB - 256 MiB)."""
+        res = {}
+        ks = range(0, 5) if SMOKE else range(0, 11)
+        ga = torch.Generator(device="cuda")
+        ga.manual_seed(3000 + rank)
+        scale = torch.exp(torch.randn(4096, device="cuda", generator=ga) * 0.5)
+        for k in ks:
+            T = 32 << k
+            a = (torch.randn(T, 4096, device="cuda", generator=ga) * scale).to(torch.bfloat16)
+            o = torch.empty_like(a)
+            nb = a.clone()
+            res[f"{2 * a.numel() >> 10}KiB"] = pair(lambda: comm.all_reduce(o, a, stream),
+                                                     lambda: dist.all_reduce(nb), 2 * a.numel())
+        return res
+
+    def c5_ag_rs():
+        """allgather (S = total output) and reduce-scatter (S = total input per rank), S = 1 MiB - 4 GiB."""
+        res = {}
+        top = 26 if SMOKE else 32
+        big = torch.empty((1 << top) // 2, dtype=torch.bfloat16, device="cuda")
+        _fill_w(big, 5000 + rank)
+        for lg in range(20, top + 1):
+            S = 1 << lg
+            el = S // 2
+            if el % (world * 8):
+                continue
+            shard = big[: el // world]
+            agout = torch.empty(el, dtype=torch.bfloat16, device="cuda")
+            res[f"allgather_{S >> 20}MiB"] = pair(lambda: comm.all_gather(agout, shard, stream),
+                                                 lambda: dist.all_gather_into_tensor(agout, shard), S)
+            del agout
+            rsin = big[:el]
+            rsout = torch.empty(el // world, dtype=torch.bfloat16, device="cuda")
+            res[f"reduce_scatter_{S >> 20}MiB"] = pair(lambda: comm.reduce_scatter(rsout, rsin, stream),
+                                                      lambda: dist.reduce_scatter_tensor(rsout, rsin), S)
+            del rsout
+        del big
+        torch.cuda.empty_cache()
+        return res
+
+    def kv_p2p():
+        """Llama-3-8B KV cache, 7680 tokens = 480 blocks x 32 layers x 64 KiB = 960 MiB bf16, pairs
+        2i -> 2i+1: one message and 32 per-layer messages of 30 MiB."""
+        layers, nb = (4, 60) if SMOKE else (32, 480)
+        gk = torch.Generator(device="cuda")
+        gk.manual_seed(8000 + rank)
+        kscale = torch.exp(torch.randn(layers, 1, 1, 8, 128, device="cuda", generator=gk) * 0.5)
+        k = torch.randn(layers, nb, 16, 8, 128, device="cuda", generator=gk) * kscale
+        v = torch.randn(layers, nb, 16, 8, 128, device="cuda", generator=gk)
+        kv = torch.stack([k, v], dim=2).to(torch.bfloat16).contiguous().view(layers, -1)
+        del k, v
+        rx = torch.empty_like(kv)
+        tot = pairs * 2 * kv.numel()
+
+        def one(u):
+            if role == "send":
+                (comm.send(kv.view(-1), peer, stream) if u else dist.send(kv.view(-1), peer))
+            elif role == "recv":
+                (comm.recv(rx.view(-1), peer, stream) if u else dist.recv(rx.view(-1), peer))
+
+        def per_layer(u):
+            for i in range(layers):
+                if role == "send":
+                    (comm.send(kv[i], peer, stream) if u else dist.send(kv[i], peer))
+                elif role == "recv":
+                    (comm.recv(rx[i], peer, stream) if u else dist.recv(rx[i], peer))
+        return {"one_message": pair(lambda: one(True), lambda: one(False), tot),
+                "per_layer": pair(lambda: per_layer(True), lambda: per_layer(False), tot),
+                "bytes_per_pair": 2 * kv.numel()}
+
+    def c3_weight_sync():
+        """Qwen2.5-7B-shaped bf16 weights (339 tensors, 15.23 GB) broadcast from rank 0 to all others:
+        per tensor and in 256 MiB buckets (uzip compressed scatter + relay vs NCCL broadcast)."""
+        h, kvd, ff, vocab = 3584, 512, 18944, 152064
+        layer = [(h, h), (h,), (kvd, h), (kvd,), (kvd, h), (kvd,), (h, h), (ff, h), (ff, h), (h, ff), (h,), (h,)]
+        shapes = [(vocab, h)] + layer * 28 + [(h,), (vocab, h)]
+        sizes = [int(torch.tensor(s).prod()) for s in shapes]
+        if SMOKE:
+            sizes = [max(8, s // 4096 // 8 * 8) for s in sizes[:20]]  # views stay 16-byte aligned
+        total = sum(sizes)
+        flat = torch.empty(total, dtype=torch.bfloat16, device="cuda")
+        if rank == 0:
+            _fill_w(flat, 7000)
+        views, o = [], 0
+        for s in sizes:
+            views.append(flat[o:o + s])
+            o += s
+        bucket = (256 * MB) // 2
+        buckets = [flat[i:i + bucket] for i in range(0, total, bucket)]
+        res = {"tensors": len(sizes), "bytes": 2 * total}
+        res["per_tensor"] = pair(lambda: [comm.broadcast(t, 0, stream) for t in views],
+                                 lambda: [dist.broadcast(t, 0) for t in views], 2 * total)
+        res["bucket_256MiB"] = pair(lambda: [comm.broadcast(t, 0, stream) for t in buckets],
+                                    lambda: [dist.broadcast(t, 0) for t in buckets], 2 * total)
+        del flat, views, buckets
+        torch.cuda.empty_cache()
+        return res
+
+    suite("c2_grid", c2_grid)
+    suite("c4_allreduce", c4_allreduce)
+    suite("c5_ag_rs", c5_ag_rs)
+    suite("kv_p2p", kv_p2p)
+    suite("c3_weight_sync", c3_weight_sync)
+    out["budget_s"] = budget
+    return out

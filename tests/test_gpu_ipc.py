@@ -35,6 +35,13 @@ def test_bench_dist_smoke_two_processes_same_gpu():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["compression_ratio"] < 0.75
+    # the BASELINE configs[1..4] sweeps the driver's multi-GPU run reports
+    su = line["suites"]
+    for k in ("c2_grid", "c4_allreduce", "c5_ag_rs", "kv_p2p", "c3_weight_sync"):
+        assert k in su and "skipped" not in su[k] and "error" not in su[k], (k, su.get(k))
+    assert su["c2_grid"]["B4096_chunk64MiB"] > 0 and su["kv_p2p"]["per_layer"]["uzip_GBps"] > 0
+    assert any(v["uzip_GBps"] for k, v in su["c5_ag_rs"].items() if k.startswith("reduce_scatter"))
+    assert line["versions"]["nccl"] and "transfer_frac" in line["roofline"]
 
 
 def test_protocol_under_random_delays():
