@@ -112,6 +112,22 @@ UZIP_API uzip_status_t uzip_decompress(const void *in, size_t in_bytes, void *ou
                               uzip_dtype_t dtype, int32_t *d_status, void *ws, size_t ws_bytes,
                               void *stream);
 
+/* Ablation baseline: the paper's staged DietGPU-style compression, Steps 1-3 of
+ * P:159-170 as separate global-memory passes -- split + one global table (Step 1), every block
+ * coded into a temporary B-byte slot (Step 2), a prefix scan and a copy that merges the blocks
+ * into one contiguous buffer (Step 3, "a third global memory write").  Same encoder and
+ * format as uzip_compress with global_table = 1 (forced here), so the streams are identical.
+ * bf16 / f16 / f32 only.  res_out (nullable, 16-byte aligned, stream bytes - 64 of room): the
+ * residual plane(s) go there instead of into `out`, and split_done (nullable cudaEvent_t) is
+ * recorded after Step 1, so the caller can move the plane into `out` with the copy engine while
+ * Steps 2-3 run (copy-engine split-send).  The workspace (uzip_staged_workspace_bytes)
+ * must be zero-filled once (uzip_workspace_init); calls leave it reusable. */
+UZIP_API size_t uzip_staged_workspace_bytes(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params);
+UZIP_API uzip_status_t uzip_compress_staged(const void *in, size_t count, uzip_dtype_t dtype, void *out,
+                                            size_t out_capacity, uint64_t *d_out_bytes, void *ws,
+                                            size_t ws_bytes, const uzip_codec_params_t *params,
+                                            void *res_out, void *split_done, void *stream);
+
 /* ---------------------------------------------------------------- communicator */
 
 typedef struct uzip_comm *uzip_comm_t;

@@ -39,7 +39,7 @@ EXPORTED = [
     "uzip_comm_init", "uzip_comm_init_all", "uzip_comm_destroy", "uzip_send", "uzip_recv", "uzip_allgather",
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
     "uzip_status_string", "uzip_version", "uzip_comm_read_staging", "uzip_broadcast",
-    "uzip_alltoall", "uzip_comm_error_detail",
+    "uzip_alltoall", "uzip_comm_error_detail", "uzip_staged_workspace_bytes", "uzip_compress_staged",
 ]
 
 
@@ -108,11 +108,15 @@ def lib() -> ctypes.CDLL:
             l.uzip_broadcast.argtypes = [vp, sz, i32, i32, vp, vp]
             l.uzip_alltoall.argtypes = [vp, vp, sz, i32, vp, vp]
             l.uzip_comm_error_detail.argtypes = [vp, vp]
+            l.uzip_staged_workspace_bytes.argtypes = [sz, i32, pp]
+            l.uzip_staged_workspace_bytes.restype = sz
+            l.uzip_compress_staged.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp, vp, vp]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
             for name in EXPORTED:
-                if name not in ("uzip_compress_bound", "uzip_workspace_bytes", "uzip_status_string", "uzip_version"):
+                if name not in ("uzip_compress_bound", "uzip_workspace_bytes", "uzip_status_string", "uzip_version",
+                                "uzip_staged_workspace_bytes"):
                     getattr(l, name).restype = i32
             _lib = l
     return _lib
@@ -124,8 +128,11 @@ def _check(st: int, where: str):
 
 
 def _stream(stream) -> ctypes.c_void_p:
+    """A torch stream, a raw cudaStream_t / CUstream handle (int), or None (torch's current stream)."""
     if stream is None:
         stream = torch.cuda.current_stream()
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
     return ctypes.c_void_p(stream.cuda_stream)
 
 
@@ -217,6 +224,36 @@ def compress(x: torch.Tensor, out: torch.Tensor | None = None, out_bytes: torch.
                              out.numel(), ctypes.c_void_p(out_bytes.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
                              ws.numel(), ctypes.byref(p), _stream(stream))
     _check(st, "uzip_compress")
+    return out, out_bytes
+
+
+def compress_staged(x: torch.Tensor, out: torch.Tensor | None = None, out_bytes: torch.Tensor | None = None,
+                    stream=None, ws: torch.Tensor | None = None, res_out: torch.Tensor | None = None,
+                    split_done=None, **params):
+    """Ablation baseline: the staged Steps 1-3 pipeline (uzip_compress_staged); the stream equals
+    compress(x, global_table=True).  split_done: optional torch.cuda.Event recorded after Step 1."""
+    dt = uz_dtype(x.dtype)
+    n = x.numel()
+    params["global_table"] = True
+    p = _params(**params)
+    cap = lib().uzip_compress_bound(n, dt, ctypes.byref(p))
+    if out is None:
+        out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    if out_bytes is None:
+        out_bytes = torch.zeros(1, dtype=torch.int64, device=x.device)
+    if ws is None:
+        ws = torch.zeros(lib().uzip_staged_workspace_bytes(n, dt, ctypes.byref(p)), dtype=torch.uint8,
+                         device=x.device)
+    if split_done is not None:
+        split_done.record(torch.cuda.current_stream() if stream is None else stream)  # torch creates it lazily
+    ev = ctypes.c_void_p(split_done.cuda_event) if split_done is not None else None
+    st = lib().uzip_compress_staged(ctypes.c_void_p(x.data_ptr() if n else 0), n, dt,
+                                    ctypes.c_void_p(out.data_ptr()), out.numel(),
+                                    ctypes.c_void_p(out_bytes.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                    ws.numel(), ctypes.byref(p),
+                                    ctypes.c_void_p(res_out.data_ptr()) if res_out is not None else None, ev,
+                                    _stream(stream))
+    _check(st, "uzip_compress_staged")
     return out, out_bytes
 
 

@@ -66,7 +66,7 @@ size_t uzip_compress_bound(size_t count, uzip_dtype_t dtype, const uzip_codec_pa
 size_t uzip_workspace_bytes(size_t count, uzip_dtype_t dtype, const uzip_codec_params_t *params) {
   StreamGeom g;
   if (resolve_geom((int)dtype, count, params, &g) != UZIP_OK) return 0;
-  return (size_t)(64 + EncWs::bytes(g.n_chunks, g.n_blocks));
+  return (size_t)(64 + EncWs::bytes(g.n_chunks, g.n_blocks, g.global));
 }
 
 uzip_status_t uzip_workspace_init(void *ws, size_t ws_bytes, void *stream) {
@@ -83,7 +83,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   if (!out || !ws || !aligned16(out) || !aligned16(ws)) return UZIP_ERR_INVALID_ARG;
   if (count > 0 && (!in || !aligned16(in))) return UZIP_ERR_INVALID_ARG;
   if (out_capacity < g.total(g.n_blocks * (uint64_t)g.B)) return UZIP_ERR_CAPACITY;
-  if (ws_bytes < 64 + EncWs::bytes(g.n_chunks, g.n_blocks)) return UZIP_ERR_CAPACITY;
+  if (ws_bytes < 64 + EncWs::bytes(g.n_chunks, g.n_blocks, g.global)) return UZIP_ERR_CAPACITY;
   // one encode job, one destination (the caller's stream buffer), no flags
   Plan p;
   memset(&p, 0, sizeof p);
@@ -101,7 +101,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   J.nd = 1;
   J.dst[0] = static_cast<uint8_t *>(out);
   J.d_out_bytes = d_out_bytes;
-  EncWs::carve(w + 64, g.n_chunks, g.n_blocks, J);
+  EncWs::carve(w + 64, g.n_chunks, g.n_blocks, g.global, J);
   p.ne = 1;
   p.n_e_items = J.ntiles;
   p.epoch = reinterpret_cast<uint32_t *>(w + 28);

@@ -107,7 +107,7 @@ uzip_status_t alloc_local(uzip_comm *c) {
   uzip_status_t st = resolve_geom(kBF16, c->L.slot_bytes / 2, &c->cfg.codec, &g);
   if (st != UZIP_OK) return st;
   c->max_chunks = g.n_chunks + 1;
-  c->ws_job_bytes = EncWs::bytes(c->max_chunks, g.n_blocks + kTileBlocks);
+  c->ws_job_bytes = EncWs::bytes(c->max_chunks, g.n_blocks + kTileBlocks, g.global);
   c->ws_bytes = 128 + (uint64_t)kMaxRanks * c->ws_job_bytes;
   if (cudaMalloc(&c->ws, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaMemset(c->ws, 0, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
@@ -158,7 +158,7 @@ uint64_t round_elems(uzip_comm *c, int dt, bool compressed, uint64_t count, Stre
     StreamGeom t;
     resolve_geom(dt, elems, &c->cfg.codec, &t);
     return t.total(t.n_blocks * (uint64_t)t.B) <= c->L.slot_bytes && t.n_tiles() + 1 <= c->L.max_tiles &&
-           t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_blocks) <= c->ws_job_bytes;
+           t.n_chunks < c->max_chunks && EncWs::bytes(t.n_chunks, t.n_blocks, t.global) <= c->ws_job_bytes;
   };
   // whole table chunks when one fits a slot and the pipe chunk, else whole tiles (a round shorter
   // than a chunk has one chunk)
@@ -219,7 +219,7 @@ void enc_job(uzip_comm *c, Plan &p, int j, int dt, const uint8_t *in, uint64_t n
   if (compressed) {
     resolve_geom(dt, n, &c->cfg.codec, &J.g);
     J.ntiles = tiles_of(J.g);
-    EncWs::carve(ws_job(c, j), J.g.n_chunks, J.g.n_blocks, J);
+    EncWs::carve(ws_job(c, j), J.g.n_chunks, J.g.n_blocks, J.g.global, J);
   } else {
     J.ntiles = std::max<uint64_t>(1, (J.raw_bytes + kRawTileBytes - 1) / kRawTileBytes);
   }

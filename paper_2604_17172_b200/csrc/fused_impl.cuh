@@ -57,7 +57,7 @@ template <int DT>
 __device__ __forceinline__ void sample_hist(const EncJob &J, uint64_t c, uint32_t part, uint32_t *hist) {
   const StreamGeom &g = J.g;
   const int tid = threadIdx.x, warp = warp_id();
-  const uint32_t len = g.sample_len(c), parts = hist_parts(len);
+  const uint32_t len = g.sample_len(c), parts = hist_parts(len, g.global);
   for (int i = tid; i < kHistWarps * 256; i += kHistThreads) hist[i] = 0;
   __syncthreads();
   constexpr uint32_t kPer = VecTraits<DT>::kSym;  // symbols per 16-byte vector
@@ -95,7 +95,38 @@ __device__ __forceinline__ void sample_hist(const EncJob &J, uint64_t c, uint32_
   uint32_t sum = 0;
 #pragma unroll
   for (int w = 0; w < kHistWarps; ++w) sum += hist[256 * w + tid];
-  J.partial[(c * kMaxHistParts + part) * 256 + tid] = sum;
+  J.partial[(c * hist_cap(g.global) + part) * 256 + tid] = sum;
+  __threadfence();  // each thread orders its own row entry before the part is counted (t_item)
+}
+
+// Sum of `parts` partial rows (all 256 threads; returns the count of symbol tid).  Warp w takes rows
+// w, w + 8, ..., each lane 8 columns as two 16-byte loads, 8 rows in flight; scr: 8 x 256 u32 of smem.
+__device__ __forceinline__ uint32_t sum_rows(const uint32_t *rows, uint32_t parts, uint32_t *scr) {
+  const int lane = threadIdx.x & 31, warp = warp_id();
+  uint32_t a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t r0 = warp; r0 < parts; r0 += 8 * kWarps) {
+    uint4 v[16];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t r = r0 + u * kWarps;
+      const uint4 *q = reinterpret_cast<const uint4 *>(rows + (uint64_t)r * 256 + 8 * lane);
+      v[2 * u] = r < parts ? ld_cg_v4(q) : make_uint4(0, 0, 0, 0);
+      v[2 * u + 1] = r < parts ? ld_cg_v4(q + 1) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a[0] += v[2 * u].x, a[1] += v[2 * u].y, a[2] += v[2 * u].z, a[3] += v[2 * u].w;
+      a[4] += v[2 * u + 1].x, a[5] += v[2 * u + 1].y, a[6] += v[2 * u + 1].z, a[7] += v[2 * u + 1].w;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) scr[warp * 256 + 8 * lane + k] = a[k];
+  __syncthreads();
+  uint32_t sum = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) sum += scr[w * 256 + threadIdx.x];
+  __syncthreads();
+  return sum;
 }
 
 // A/B path (UZIP_TABLE_KERNELS=1): the same table build as two launches ahead of k_fused.
@@ -106,7 +137,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ P
   const EncJob &J = P.e[blockIdx.z];
   if (J.raw) return;
   const uint32_t part = blockIdx.x, c = blockIdx.y;
-  if (c >= J.g.n_chunks || part >= hist_parts(J.g.sample_len(c))) return;
+  if (c >= J.g.n_chunks || part >= hist_parts(J.g.sample_len(c), J.g.global)) return;
   sample_hist<DT>(J, c, part, hist);
 }
 
@@ -161,6 +192,7 @@ __device__ __forceinline__ void norm_tables(uint32_t cnt, uint4 *enc, uint16_t *
   enc[tid] = ent;
   tab16[tid] = (uint16_t)f;
   if (tab) tab[tid] = ent;
+  __threadfence();  // each thread's entries are visible GPU-wide before the caller's flag release
   __syncthreads();  // red32 / red64 free again; tab complete
 }
 
@@ -168,19 +200,19 @@ template <int DT>
 __global__ void __launch_bounds__(256) k_norm(const __grid_constant__ Plan P) {
   __shared__ unsigned long long red64[8];
   __shared__ uint32_t red32[8];
+  __shared__ uint32_t scr[kWarps * 256];
   const EncJob &J = P.e[blockIdx.y];
   if (J.raw) return;
   const StreamGeom &g = J.g;
   const int tid = threadIdx.x;
   const uint32_t c = blockIdx.x;
   if (c >= g.n_chunks) return;
-  const uint32_t parts = hist_parts(g.sample_len(c));
-  uint32_t sum = 0;
-  for (uint32_t p = 0; p < parts; ++p) sum += J.partial[((uint64_t)c * kMaxHistParts + p) * 256 + tid];
+  const uint32_t parts = hist_parts(g.sample_len(c), g.global), cap = hist_cap(g.global);
+  const uint32_t sum = sum_rows(J.partial + (uint64_t)c * cap * 256, parts, scr);
   norm_tables(sum, J.enc + c * 256, J.tab16 + c * 256, nullptr, red64, red32);
   if (tid == 0) {
     __threadfence();
-    st_release_gpu_u32(J.tflag + c, (*P.epoch & kEpochMask) + 1u);
+    st_release_gpu_u64(J.tflag + c, kCtlTag | ((*P.epoch & kEpochMask) + 1u));
   }
 }
 
@@ -260,11 +292,12 @@ static __device__ bool wait_credit(const Plan &P, const unsigned long long *cr, 
   }
 }
 
-// Poll a 32-bit flag until it equals `want` (gpu scope: a flag of this launch on this GPU).
-static __device__ bool wait_u32(const Plan &P, const uint32_t *f, uint32_t want, unsigned long long &seen) {
+// Poll a 64-bit flag until it equals `want` (gpu scope: a flag of this launch on this GPU).
+static __device__ bool wait_u64(const Plan &P, const unsigned long long *f, unsigned long long want,
+                                unsigned long long &seen) {
   unsigned long long t0 = 0;
   for (int spin = 0;; ++spin) {
-    const uint32_t v = ld_acquire_gpu_u32(f);
+    const unsigned long long v = ld_acquire_gpu_u64(f);
     if (v == want) return true;
     if ((spin & 63) == 63) {
       if (ld_volatile_u32(P.err)) return false;
@@ -272,7 +305,7 @@ static __device__ bool wait_u32(const Plan &P, const uint32_t *f, uint32_t want,
       if (t0 == 0) t0 = now;
       else if (now - t0 > P.timeout_ns) {
         seen = v;
-        raise_err_at(P, UZIP_ERR_TIMEOUT, 5, want, v, (uint64_t)(uintptr_t)f);
+        raise_err_at(P, UZIP_ERR_TIMEOUT, 5, (uint32_t)want, v, (uint64_t)(uintptr_t)f);
         return false;
       }
     }
@@ -299,7 +332,8 @@ static __device__ unsigned long long lookback_finish(const Plan &P, unsigned lon
   for (int spin = 0;; ++spin) {
     const int64_t idx = base - lane;
     unsigned long long s = idx >= 0 ? ld_relaxed_u64(&status[idx]) : (kFlagInc | eb);
-    const uint32_t flag = (s & emask) == eb ? (uint32_t)(s >> 62) : 0u;  // another launch's word: not ready
+    uint32_t flag = (s & emask) == eb ? (uint32_t)(s >> 62) : 0u;  // another launch's word: not ready
+    flag = flag == 3 ? 0u : flag;                                    // a control word (kCtlTag): not ready
     const uint32_t inc = __ballot_sync(0xFFFFFFFFu, flag == 2);
     const uint32_t notready = __ballot_sync(0xFFFFFFFFu, flag == 0);
     const int first_inc = inc ? __ffs(inc) - 1 : 31;
@@ -716,28 +750,28 @@ static __device__ void t_item(const Plan &P, const EncJob &J, uint64_t c, uint32
   const int tid = threadIdx.x;
   uint32_t *hist = reinterpret_cast<uint32_t *>(smem + C::kEncTab);  // the warp buffers (free between items)
   sample_hist<DT>(J, c, part, hist);
-  const uint32_t parts = hist_parts(J.g.sample_len(c)), ep = S.epoch;
+  const uint32_t parts = hist_parts(J.g.sample_len(c), J.g.global), cap = hist_cap(J.g.global), ep = S.epoch;
   __syncthreads();
   if (tid == 0) {
     __threadfence();  // the partial is visible before it is counted
-    uint32_t old = ld_volatile_u32(J.tcount + c), want;
+    const unsigned long long tag = kCtlTag | ((unsigned long long)ep << 32);
+    unsigned long long old = J.tcount[c], want;  // tag | parts counted
     for (;;) {
-      want = (old >> 8) == ep ? old + 1u : ((ep << 8) | 1u);  // first part of this launch restarts the count
-      const uint32_t seen = atomicCAS(J.tcount + c, old, want);
+      want = (old & ~0xFFFFFFFFull) == tag ? old + 1ull : (tag | 1ull);  // the first part of a launch restarts
+      const unsigned long long seen = atomicCAS(J.tcount + c, old, want);
       if (seen == old) break;
       old = seen;
     }
-    S.is_last = (want & 0xFFu) == parts ? 1u : 0u;
+    S.is_last = (uint32_t)want == parts ? 1u : 0u;
     __threadfence();
   }
   __syncthreads();
   if (!S.is_last) return;
-  uint32_t sum = 0;
-  for (uint32_t p = 0; p < parts; ++p) sum += ld_cg_u32(J.partial + (c * kMaxHistParts + p) * 256 + tid);
+  const uint32_t sum = sum_rows(J.partial + c * cap * 256, parts, hist);
   norm_tables(sum, J.enc + c * 256, J.tab16 + c * 256, nullptr, S.red64, S.red);
   if (tid == 0) {
     __threadfence();
-    st_release_gpu_u32(J.tflag + c, ep + 1u);
+    st_release_gpu_u64(J.tflag + c, kCtlTag | (ep + 1u));
   }
 }
 
@@ -946,7 +980,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
     if (!P.tables_ready) {
       if (tid == 0) {  // the chunk's table: published by its last T item (a smaller ticket)
         unsigned long long seen = 0;
-        S.abort = wait_u32(P, J.tflag + c, S.epoch + 1u, seen) ? 0u : 1u;
+        S.abort = wait_u64(P, J.tflag + c, kCtlTag | (S.epoch + 1u), seen) ? 0u : 1u;
       }
       __syncthreads();
       if (S.abort) return;
@@ -1382,7 +1416,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     const uint64_t ca = ga.n_blocks ? chunk_of(ga, b0) : 0;
     const uint64_t key = ((uint64_t)P.ag_job << 48) | ca;
     uint4 *tab = reinterpret_cast<uint4 *>(smem);
-    uint32_t *tabflag = A.tflag;  // per chunk: epoch + 1 = table published
+    unsigned long long *tabflag = A.tflag;  // per chunk: kCtlTag | (epoch + 1) = table published
     if (ga.n_blocks && (uint32_t)b0 % ga.CB == 0) {
       // the chunk's first tile is its sample (R26): histogram the symbols just split, rule N1, publish
       uint32_t *hist = dtab;  // 8 x 256 counters in the decode-table region
@@ -1404,13 +1438,13 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
       norm_tables(cnt, A.enc + ca * 256, A.tab16 + ca * 256, tab, S.red64, S.red);
       if (tid == 0) {
         __threadfence();
-        st_release_gpu_u32(tabflag + ca, S.epoch + 1u);
+        st_release_gpu_u64(tabflag + ca, kCtlTag | (S.epoch + 1u));
       }
       enc_key = key;
     } else if (ga.n_blocks && key != enc_key) {
       if (tid == 0) {  // the chunk's first tile (a smaller ticket) publishes the table
         unsigned long long v = 0;
-        S.abort = wait_u32(P, tabflag + ca, S.epoch + 1u, v) ? 0u : 1u;
+        S.abort = wait_u64(P, tabflag + ca, kCtlTag | (S.epoch + 1u), v) ? 0u : 1u;
       }
       __syncthreads();
       if (S.abort) return;
@@ -1541,7 +1575,7 @@ cudaError_t launch_tables_t(const Plan &p, cudaStream_t st) {
     if (J.raw) continue;
     max_chunks = J.g.n_chunks > max_chunks ? J.g.n_chunks : max_chunks;
     for (uint64_t c = 0; c < J.g.n_chunks; c += (J.g.n_chunks > 1 ? J.g.n_chunks - 1 : 1)) {
-      const uint32_t parts = hist_parts(J.g.sample_len(c));
+      const uint32_t parts = hist_parts(J.g.sample_len(c), J.g.global);
       max_parts = parts > max_parts ? parts : max_parts;
     }
   }

@@ -49,9 +49,9 @@ struct EncJob {
   uint4 *enc;                               // per-chunk encode entries (k_norm)
   uint16_t *tab16;                          // per-chunk serialized tables (k_norm)
   unsigned long long *tile_status;          // per-tile look-back words (zeroed by k_hist)
-  uint32_t *partial;                        // partial histograms [chunk][kMaxHistParts][256]
-  uint32_t *tflag;                          // per chunk: table published = epoch + 1
-  uint32_t *tcount;                         // per chunk: (epoch << 8) | parts done (T items)
+  uint32_t *partial;                        // [chunk][hist_cap(global)][256] partial counts, a row per part
+  unsigned long long *tflag;                // per chunk: table published = kCtlTag | (epoch + 1)
+  unsigned long long *tcount;               // per chunk: kCtlTag | epoch << 32 | parts done (T items)
   uint64_t *d_out_bytes;                    // codec: stream size (may be null)
   unsigned long long *wire_acc;             // comm: += stream bytes x nd (may be null)
 };
@@ -134,22 +134,29 @@ struct CreditWait {
   uint64_t timeout_ns;
 };
 
-// k_hist splits a chunk's sample over up to kMaxHistParts CTAs of >= 16 Ki symbols.
-constexpr uint32_t kMaxHistParts = 64;
-__host__ __device__ inline uint32_t hist_parts(uint32_t sample_len) {
-  const uint32_t p = (sample_len + 16383) / 16384;
-  return p < 1 ? 1 : (p > kMaxHistParts ? kMaxHistParts : p);
+// A chunk's sample is split over parts of >= 16 Ki symbols, at most hist_cap(global) of them (64 per
+// chunk; the global-table mode samples the whole stream as one chunk: up to 512).
+// Every part writes its own row of partial counts, so no state needs clearing between launches
+// (a workspace may be reused for streams of other sizes, whose layout puts other data there).
+__host__ __device__ inline uint32_t hist_cap(uint32_t global) { return global ? 512u : 64u; }
+__host__ __device__ inline uint32_t hist_parts(uint32_t sample_len, uint32_t global) {
+  const uint32_t p = (sample_len + 16383) / 16384, cap = hist_cap(global);
+  return p < 1 ? 1 : (p > cap ? cap : p);
 }
+// Table flags and part counters are 64-bit words tagged with the top two bits set, a value no other
+// workspace word ever holds (look-back words use flags 1 and 2 there; counts, tables and entries
+// stay below 2^62), so a stale word of an earlier, differently laid-out call can never match.
+constexpr unsigned long long kCtlTag = 3ull << 62;
 
 // Workspace of one encode job: enc entries, serialized tables, look-back
 // words, partial histograms (all written by k_hist/k_norm before use: no state
 // survives a launch, so the layout may change from call to call).
 struct EncWs {
-  static uint64_t bytes(uint64_t n_chunks, uint64_t n_blocks) {
+  static uint64_t bytes(uint64_t n_chunks, uint64_t n_blocks, uint32_t global) {
     return round16(4096 * n_chunks) + round16(512 * n_chunks) + round16(8 * (n_blocks + 1)) +
-           round16(1024ull * kMaxHistParts * n_chunks) + 2 * round16(4 * n_chunks);
+           round16(1024ull * hist_cap(global) * n_chunks) + 2 * round16(8 * n_chunks);
   }
-  static void carve(uint8_t *p, uint64_t n_chunks, uint64_t n_blocks, EncJob &j) {
+  static void carve(uint8_t *p, uint64_t n_chunks, uint64_t n_blocks, uint32_t global, EncJob &j) {
     j.enc = reinterpret_cast<uint4 *>(p);
     p += round16(4096 * n_chunks);
     j.tab16 = reinterpret_cast<uint16_t *>(p);
@@ -157,22 +164,22 @@ struct EncWs {
     j.tile_status = reinterpret_cast<unsigned long long *>(p);
     p += round16(8 * (n_blocks + 1));
     j.partial = reinterpret_cast<uint32_t *>(p);
-    p += round16(1024ull * kMaxHistParts * n_chunks);
-    j.tflag = reinterpret_cast<uint32_t *>(p);
-    p += round16(4 * n_chunks);
-    j.tcount = reinterpret_cast<uint32_t *>(p);
+    p += round16(1024ull * hist_cap(global) * n_chunks);
+    j.tflag = reinterpret_cast<unsigned long long *>(p);
+    p += round16(8 * n_chunks);
+    j.tcount = reinterpret_cast<unsigned long long *>(p);
   }
 };
 
-// T items of an encode job: every chunk's sample split into hist_parts(sample) parts (all chunks but
+// T items of an encode job: every chunk's sample split into hist_parts(sample, global) parts (all chunks but
 // the last have the same sample length).
 __host__ __device__ inline uint64_t t_items_of(const EncJob &J) {
   if (J.raw || J.g.n_blocks == 0) return 0;
   const uint64_t nc = J.g.n_chunks;
-  return (nc - 1) * hist_parts(J.g.sample_len(0)) + hist_parts(J.g.sample_len(nc - 1));
+  return (nc - 1) * hist_parts(J.g.sample_len(0), J.g.global) + hist_parts(J.g.sample_len(nc - 1), J.g.global);
 }
 __host__ __device__ inline void t_item_at(const EncJob &J, uint64_t k, uint64_t &c, uint32_t &part) {
-  const uint64_t nc = J.g.n_chunks, pf = hist_parts(J.g.sample_len(0));
+  const uint64_t nc = J.g.n_chunks, pf = hist_parts(J.g.sample_len(0), J.g.global);
   if (k < (nc - 1) * pf) {
     c = k / pf;
     part = (uint32_t)(k % pf);

@@ -130,10 +130,129 @@ def main():
                                   "wire_ratio": round(wire / raw, 5),
                                   "note": "uzip_compress + device copy of the stream + uzip_decompress, serial"}
     print("encode_send", res["legs"]["encode_send"], flush=True)
+    codec_legs(uz, x, args, timed, res)
     line = json.dumps(res)
     print(line)
     if args.out:
         open(args.out, "w").write(line + "\n")
+
+
+def codec_legs(uz, x, args, timed, res):
+    """Compression side alone (1 GiB bf16 W, one GPU), fused vs the paper's staged pipeline:
+      * fused_local / fused_global: uzip_compress with per-chunk sampled tables (default) and with one
+        global table (global_table = 1);
+      * staged_3pass: uzip_compress_staged -- Step 1 split + global histogram, Step 2 every block into a
+        temporary slot, Step 3 scan + copy into one buffer (P:159-170); same stream as fused_global;
+      * staged_ce_split_send: the same with the residual plane written to a side buffer and moved into
+        the stream by the copy engine (cudaMemcpyAsync on a second stream after Step 1) while Steps 2-3
+        run -- the split-send of P:300-311 on copy engines;
+      * green_ctx_<k>sm: fused_local in a Green Context of k SMs (cuGreenCtxCreate), the paper's
+        SM-limited runs (fig:resource_usage)."""
+    import torch
+    n = x.numel()
+    raw = 2 * n
+    stream = torch.cuda.Stream()
+    cap = uz.compress_bound(n, uz.BF16)
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    legs = {}
+
+    def leg(name, step, ref=None):
+        ms = timed(step, stream)
+        torch.cuda.synchronize()
+        got = out[: int(nb.item())].cpu().numpy().tobytes() if ref is not None else None
+        legs[name] = {"GBps_uncompressed": round(raw / (ms / 1e3) / GB, 2), "ms": round(ms, 4),
+                      "ratio": round(int(nb.item()) / raw, 5)}
+        if ref is not None:
+            legs[name]["bytes_equal_fused_global"] = got == ref
+        print(name, legs[name], flush=True)
+
+    ws = uz.Workspace(0).get(max(uz.workspace_bytes(n, uz.BF16, global_table=True), uz.workspace_bytes(n, uz.BF16)),
+                             stream)
+
+    def fused(glob):
+        def step():
+            with torch.cuda.stream(stream):
+                uz.compress(x, out=out, out_bytes=nb, stream=stream, ws=ws, global_table=glob)
+        return step
+    leg("fused_local", fused(False))
+    leg("fused_global", fused(True))
+    ref = out[: int(nb.item())].cpu().numpy().tobytes()
+    sws = torch.zeros(uz.lib().uzip_staged_workspace_bytes(n, uz.BF16, None), dtype=torch.uint8, device="cuda")
+
+    def staged():
+        with torch.cuda.stream(stream):
+            uz.compress_staged(x, out=out, out_bytes=nb, stream=stream, ws=sws)
+    leg("staged_3pass", staged, ref)
+    side = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ev = torch.cuda.Event()
+    s2 = torch.cuda.Stream()
+
+    def staged_ce():
+        with torch.cuda.stream(stream):
+            uz.compress_staged(x, out=out, out_bytes=nb, stream=stream, ws=sws, res_out=side, split_done=ev)
+        s2.wait_event(ev)
+        with torch.cuda.stream(s2):
+            out[64:64 + n].copy_(side, non_blocking=True)  # the copy engine moves the residual plane
+        stream.wait_stream(s2)
+    leg("staged_ce_split_send", staged_ce, ref)
+    res["codec_legs"] = legs
+    try:
+        res["green_ctx"] = green_ctx_legs(uz, x, args)
+    except Exception as e:  # report, do not fail the other legs
+        res["green_ctx"] = {"error": repr(e)[:300]}
+    print("green_ctx", res["green_ctx"], flush=True)
+
+
+def green_ctx_legs(uz, x, args):
+    """uzip_compress in Green Contexts holding k of the GPU's SMs (driver API through cuda-python)."""
+    import torch
+    from cuda.bindings import driver as d
+
+    def ok(r):
+        if not isinstance(r, tuple):
+            r = (r,)
+        if int(r[0]) != 0:
+            raise RuntimeError(f"driver error {r[0]}")
+        return None if len(r) == 1 else (r[1] if len(r) == 2 else r[1:])
+
+    ok(d.cuInit(0))
+    dev = ok(d.cuDeviceGet(0))
+    sm_res = ok(d.cuDeviceGetDevResource(dev, d.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM))
+    n = x.numel()
+    raw = 2 * n
+    cap = uz.compress_bound(n, uz.BF16)
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = uz.Workspace(0).get(uz.workspace_bytes(n, uz.BF16))
+    prim = ok(d.cuCtxGetCurrent())
+    res = {}
+    for k in (16, 32, 64, 128):  # SMs per green context
+        groups, ngroups, _rem = ok(d.cuDevSmResourceSplitByCount(1, sm_res, 0, k))
+        desc = ok(d.cuDevResourceGenerateDesc([groups[0]] if isinstance(groups, list) else groups, 1))
+        gctx = ok(d.cuGreenCtxCreate(desc, dev, d.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM))
+        gst = ok(d.cuGreenCtxStreamCreate(gctx, d.CUstream_flags.CU_STREAM_NON_BLOCKING, 0))
+        got_sm = ok(d.cuGreenCtxGetDevResource(gctx, d.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM))
+        ctx = ok(d.cuCtxFromGreenCtx(gctx))
+        ok(d.cuCtxSetCurrent(ctx))
+        try:
+            sp = int(gst)
+            for _ in range(2):
+                uz.compress(x, out=out, out_bytes=nb, stream=sp, ws=ws)
+            ok(d.cuStreamSynchronize(gst))
+            e0, e1 = ok(d.cuEventCreate(0)), ok(d.cuEventCreate(0))
+            ok(d.cuEventRecord(e0, gst))
+            for _ in range(args.steps):
+                uz.compress(x, out=out, out_bytes=nb, stream=sp, ws=ws)
+            ok(d.cuEventRecord(e1, gst))
+            ok(d.cuEventSynchronize(e1))
+            ms = ok(d.cuEventElapsedTime(e0, e1)) / args.steps
+            res[f"green_ctx_{k}sm"] = {"sms": int(got_sm.sm.smCount), "compress_GBps_uncompressed":
+                                       round(raw / (ms / 1e3) / GB, 2), "ms": round(ms, 4)}
+        finally:
+            ok(d.cuCtxSetCurrent(prim))
+            d.cuGreenCtxDestroy(gctx)
+    return res
 
 
 if __name__ == "__main__":

@@ -309,3 +309,35 @@ def test_stored_raw_tie_equals_oracle(uz, orc, kind):
     assert got == ref
     st, back = gpu_decompress(uz, got, bits.size, BF16)
     assert st == 0 and np.array_equal(back, bits)
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("n", [3, 4096, 3 * 4096 + 17, 41 * 4096 + 5])
+@pytest.mark.parametrize("B", [1024, 4096])
+def test_staged_pipeline_equals_oracle_global(uz, orc, dtype, n, B):
+    """Ablation baseline (f3): the staged Steps 1-3 pipeline writes the oracle's
+    global-table stream byte for byte -- also with the residual plane redirected to a side buffer
+    and moved into the stream afterwards (the copy-engine split-send variant)."""
+    bits = synth.normal(n, 0.02, 300 + n, dtype)
+    if n > 4096 * 8:
+        bits[4096 * 2:4096 * 3] = synth.random_bits(4096, 9, dtype)  # stored-raw blocks too
+    ref = orc.compress(dtype, bits, global_table=True, block_symbols=B)
+    x = torch.from_numpy(bits.view(NPV[dtype]).copy()).view(TD[dtype]).cuda()
+    out, nb = uz.compress_staged(x, block_symbols=B)
+    torch.cuda.synchronize()
+    assert out[: int(nb.item())].cpu().numpy().tobytes() == ref
+    # copy-engine variant: residual plane to a side buffer, moved after Step 1 on a second stream
+    side = torch.empty(len(ref), dtype=torch.uint8, device="cuda")
+    ev = torch.cuda.Event()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out2 = torch.zeros_like(out)
+    with torch.cuda.stream(s1):
+        _, nb2 = uz.compress_staged(x, out=out2, stream=s1, res_out=side, split_done=ev, block_symbols=B)
+    res_bytes = orc.sections(ref)["off_tab"] - 64
+    with torch.cuda.stream(s2):
+        s2.wait_event(ev)
+        out2[64:64 + res_bytes].copy_(side[:res_bytes], non_blocking=True)
+    torch.cuda.synchronize()
+    got = out2[: int(nb2.item())].cpu().numpy()
+    got[64 + res_bytes:orc.sections(ref)["off_tab"]] = 0  # alignment pad after the plane (none for whole blocks)
+    assert got.tobytes() == ref
