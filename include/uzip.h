@@ -128,6 +128,14 @@ UZIP_API uzip_status_t uzip_compress_staged(const void *in, size_t count, uzip_d
                                             size_t ws_bytes, const uzip_codec_params_t *params,
                                             void *res_out, void *split_done, void *stream);
 
+/* NVLink SHARP multicast: *supported = CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED of
+ * `device` (0 when the driver lacks multicast).  uzip_nvls_selftest creates a one-device multicast
+ * object of >= `bytes`, binds device memory, stores a pattern through multimem.st and checks it
+ * through the unicast mapping: UZIP_OK, UZIP_ERR_NOT_IMPLEMENTED (no multicast, or the node refuses to
+ * create a multicast object), or an error. */
+UZIP_API uzip_status_t uzip_nvls_supported(int device, int *supported);
+UZIP_API uzip_status_t uzip_nvls_selftest(int device, size_t bytes);
+
 /* ---------------------------------------------------------------- communicator */
 
 typedef struct uzip_comm *uzip_comm_t;

@@ -40,6 +40,7 @@ EXPORTED = [
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
     "uzip_status_string", "uzip_version", "uzip_comm_read_staging", "uzip_broadcast",
     "uzip_alltoall", "uzip_comm_error_detail", "uzip_staged_workspace_bytes", "uzip_compress_staged",
+    "uzip_nvls_supported", "uzip_nvls_selftest",
 ]
 
 
@@ -111,6 +112,8 @@ def lib() -> ctypes.CDLL:
             l.uzip_staged_workspace_bytes.argtypes = [sz, i32, pp]
             l.uzip_staged_workspace_bytes.restype = sz
             l.uzip_compress_staged.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp, vp, vp]
+            l.uzip_nvls_supported.argtypes = [i32, ctypes.POINTER(i32)]
+            l.uzip_nvls_selftest.argtypes = [i32, sz]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
@@ -275,6 +278,17 @@ def decompress(stream_buf: torch.Tensor, count: int, dtype, out: torch.Tensor | 
                                _stream(stream))
     _check(st, "uzip_decompress")
     return out, status
+
+
+def nvls_supported(device: int = 0) -> bool:
+    v = ctypes.c_int(0)
+    _check(lib().uzip_nvls_supported(device, ctypes.byref(v)), "uzip_nvls_supported")
+    return bool(v.value)
+
+
+def nvls_selftest(device: int = 0, nbytes: int = 4 << 20) -> int:
+    """Status of the one-device multicast self-test (OK, NOT_IMPLEMENTED without multicast)."""
+    return lib().uzip_nvls_selftest(device, nbytes)
 
 
 def status_string(st: int) -> str:

@@ -191,6 +191,23 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t *p) {
 __device__ __forceinline__ void st_release_gpu_u32(uint32_t *p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// NVLS multicast stores (f1): one store to a multicast address is replicated by the NVSwitch into
+// every GPU bound to the multicast object (bit patterns travel unchanged: .f32 is only the width).
+__device__ __forceinline__ void mc_store_v4(void *mc, uint4 v) {
+  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_store_v2(void *mc, uint2 v) {
+  asm volatile("multimem.st.weak.global.v2.f32 [%0], {%1, %2};" ::"l"(mc), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void mc_store_b32(void *mc, uint32_t v) {
+  asm volatile("multimem.st.weak.global.b32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+// Release of a tile flag to every bound GPU after the tile's multicast data stores.
+__device__ __forceinline__ void mc_release_sys_u64(void *mc, unsigned long long v) {
+  asm volatile("fence.proxy.alias;\n\tmultimem.st.release.sys.global.b64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
   uint32_t r;
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");

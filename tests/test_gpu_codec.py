@@ -341,3 +341,15 @@ def test_staged_pipeline_equals_oracle_global(uz, orc, dtype, n, B):
     got = out2[: int(nb2.item())].cpu().numpy()
     got[64 + res_bytes:orc.sections(ref)["off_tab"]] = 0  # alignment pad after the plane (none for whole blocks)
     assert got.tobytes() == ref
+
+
+def test_nvls_multicast_primitive(uz):
+    """f1 building block: a one-device NVLS multicast object -- multimem.st through the multicast
+    mapping lands in the bound memory (checked through the unicast mapping).  Skips when the GPU /
+    driver reports no multicast support (the fan-out then stays unicast)."""
+    if not uz.nvls_supported(0):
+        pytest.skip("no multicast support on this device")
+    st = uz.nvls_selftest(0, 8 << 20)
+    if st == uz.ERR_NOT_IMPLEMENTED:
+        pytest.skip("cuMulticastCreate refused on this node (single visible GPU / no multicast team)")
+    assert st == 0
