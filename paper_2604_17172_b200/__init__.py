@@ -109,15 +109,18 @@ def lib() -> ctypes.CDLL:
             l.uzip_broadcast.argtypes = [vp, sz, i32, i32, vp, vp]
             l.uzip_alltoall.argtypes = [vp, vp, sz, i32, vp, vp]
             l.uzip_comm_error_detail.argtypes = [vp, vp]
-            l.uzip_staged_workspace_bytes.argtypes = [sz, i32, pp]
-            l.uzip_staged_workspace_bytes.restype = sz
-            l.uzip_compress_staged.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp, vp, vp]
-            l.uzip_nvls_supported.argtypes = [i32, ctypes.POINTER(i32)]
-            l.uzip_nvls_selftest.argtypes = [i32, sz]
+            if hasattr(l, "uzip_compress_staged"):  # (older builds, loaded as tuning variants, lack these)
+                l.uzip_staged_workspace_bytes.argtypes = [sz, i32, pp]
+                l.uzip_staged_workspace_bytes.restype = sz
+                l.uzip_compress_staged.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp, vp, vp]
+                l.uzip_nvls_supported.argtypes = [i32, ctypes.POINTER(i32)]
+                l.uzip_nvls_selftest.argtypes = [i32, sz]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
             for name in EXPORTED:
+                if not hasattr(l, name):
+                    continue
                 if name not in ("uzip_compress_bound", "uzip_workspace_bytes", "uzip_status_string", "uzip_version",
                                 "uzip_staged_workspace_bytes"):
                     getattr(l, name).restype = i32

@@ -13,11 +13,13 @@ using namespace uzip;
 namespace uzip {
 
 bool table_kernels(uint64_t n_chunks) {
-  // UZIP_TABLE_KERNELS=1: the two table launches (A/B); default: T items inside k_fused, which save
-  // two dependent launches (C1 4 MiB: 25 vs 33 us per compress) and cost nothing at 1 GiB.
-  (void)n_chunks;  // by size: measured equal at 1 GiB (0.7265 ms either way), so T items everywhere
-  static const int v = getenv("UZIP_TABLE_KERNELS") ? atoi(getenv("UZIP_TABLE_KERNELS")) : 0;
-  return v != 0;
+  // UZIP_TABLE_KERNELS=1 / 0 forces the two table launches / the T items.  By default small streams
+  // (< kTableKernelChunks chunks) use T items, which save two dependent launches (C1 4 MiB compress:
+  // 25 vs 33 us), and large ones the launches, which spare every E item the table-flag poll (1 GiB
+  // codec: equal, 0.7265 ms either way; loopback 1 GiB P2P: 2.15 vs 2.37 ms).
+  static const int v = getenv("UZIP_TABLE_KERNELS") ? atoi(getenv("UZIP_TABLE_KERNELS")) : -1;
+  if (v >= 0) return v != 0;
+  return n_chunks >= kTableKernelChunks;
 }
 
 uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g) {

@@ -96,7 +96,6 @@ __device__ __forceinline__ void sample_hist(const EncJob &J, uint64_t c, uint32_
 #pragma unroll
   for (int w = 0; w < kHistWarps; ++w) sum += hist[256 * w + tid];
   J.partial[(c * hist_cap(g.global) + part) * 256 + tid] = sum;
-  __threadfence();  // each thread orders its own row entry before the part is counted (t_item)
 }
 
 // Sum of `parts` partial rows (all 256 threads; returns the count of symbol tid).  Warp w takes rows
@@ -192,8 +191,9 @@ __device__ __forceinline__ void norm_tables(uint32_t cnt, uint4 *enc, uint16_t *
   enc[tid] = ent;
   tab16[tid] = (uint16_t)f;
   if (tab) tab[tid] = ent;
-  __threadfence();  // each thread's entries are visible GPU-wide before the caller's flag release
-  __syncthreads();  // red32 / red64 free again; tab complete
+  // red32 / red64 free again; tab complete.  The caller's thread 0 then fences and releases the
+  // chunk's flag: bar.sync + one gpu-scope fence cover every thread's stores (the grid-sync pattern)
+  __syncthreads();
 }
 
 template <int DT>
@@ -673,6 +673,23 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
   ovf = over;
 }
 
+// Exclusive prefix (roff) of the 8 per-warp block sizes of a tile at this warp, its own size and the
+// tile's total: one shared load per lane and a 3-step shuffle scan instead of a loop over the warps.
+__device__ __forceinline__ void tile_prefix(const uint32_t *sizes, int warp, uint32_t &roff, uint32_t &mine,
+                                            uint32_t *total = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t v = lane < kWarps ? sizes[lane] : 0u;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < kWarps; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  roff = __shfl_sync(0xFFFFFFFFu, incl - v, warp);
+  mine = __shfl_sync(0xFFFFFFFFu, v, warp);
+  if (total) *total = __shfl_sync(0xFFFFFFFFu, incl, kWarps - 1);
+}
+
 // A coded tile whose payload waits in the CTA's ring for its offset: the
 // tile's aggregate is published as soon as it is coded, the look-back is
 // finished one tile later (when every predecessor has long been coded), so
@@ -698,9 +715,8 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
   if (tile_off != ~0ull) {
     const uint64_t b0 = t * kTileBlocks, b = b0 + warp;
     const uint64_t c = chunk_of(g, b0);
-    uint32_t roff = 0;
-    for (int w = 0; w < warp; ++w) roff += S.psize[w];
-    const uint32_t size = S.psize[warp];
+    uint32_t roff, size;
+    tile_prefix(S.psize, warp, roff, size);
     if (b < g.n_blocks) {
       const unsigned long long off = tile_off + roff;
       for (uint32_t d = 0; d < J.nd; ++d) {
@@ -753,9 +769,9 @@ static __device__ void t_item(const Plan &P, const EncJob &J, uint64_t c, uint32
   const uint32_t parts = hist_parts(J.g.sample_len(c), J.g.global), cap = hist_cap(J.g.global), ep = S.epoch;
   __syncthreads();
   if (tid == 0) {
-    __threadfence();  // the partial is visible before it is counted
+    __threadfence();  // after the barrier: every thread's partial row is visible before it is counted
     const unsigned long long tag = kCtlTag | ((unsigned long long)ep << 32);
-    unsigned long long old = J.tcount[c], want;  // tag | parts counted
+    unsigned long long old = ld_volatile_u64(J.tcount + c), want;  // tag | parts counted (L2, not L1)
     for (;;) {
       want = (old & ~0xFFFFFFFFull) == tag ? old + 1ull : (tag | 1ull);  // the first part of a launch restarts
       const unsigned long long seen = atomicCAS(J.tcount + c, old, want);
@@ -767,7 +783,12 @@ static __device__ void t_item(const Plan &P, const EncJob &J, uint64_t c, uint32
   }
   __syncthreads();
   if (!S.is_last) return;
+#ifdef UZIP_SIMPLE_SUM
+  uint32_t sum = 0;
+  for (uint32_t p = 0; p < parts; ++p) sum += ld_cg_u32(J.partial + (c * cap + p) * 256 + tid);
+#else
   const uint32_t sum = sum_rows(J.partial + c * cap * 256, parts, hist);
+#endif
   norm_tables(sum, J.enc + c * 256, J.tab16 + c * 256, nullptr, S.red64, S.red);
   if (tid == 0) {
     __threadfence();
@@ -834,12 +855,9 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
   if (pd.job >= 0) resolve_pending<DT, B>(P, S, ring, pd);  // the previous tile's offset is due now
 
   // ---- a5: tile prefix by decoupled look-back
-  uint32_t sum = 0, roff = 0, anyovf = 0;
-  for (int w = 0; w < kWarps; ++w) {
-    if (w < warp) roff += S.size[w];
-    sum += S.size[w];
-    anyovf |= S.ovf[w];
-  }
+  uint32_t sum, roff, mine;
+  tile_prefix(S.size, warp, roff, mine, &sum);
+  const uint32_t anyovf = __any_sync(0xFFFFFFFFu, (lane < kWarps) && S.ovf[lane & (kWarps - 1)]);
   if (g.n_blocks && !anyovf && sum <= (uint32_t)ring_bytes) {
     // park the coded tile in the ring, publish its aggregate, go on coding
     if (b < g.n_blocks) {
@@ -874,8 +892,7 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
   if (tile_off == ~0ull) return;  // aborted (timeout / peer error)
 
   if (b < g.n_blocks) {
-    unsigned long long off = tile_off;
-    for (int w = 0; w < warp; ++w) off += S.size[w];
+    const unsigned long long off = tile_off + roff;
     for (uint32_t d = 0; d < J.nd; ++d) {
       uint8_t *o = J.dst[d] + g.off_pay + off;
       if (lane == 0) {

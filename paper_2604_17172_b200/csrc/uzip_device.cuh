@@ -208,6 +208,11 @@ __device__ __forceinline__ void mc_store_b32(void *mc, uint32_t v) {
 __device__ __forceinline__ void mc_release_sys_u64(void *mc, unsigned long long v) {
   asm volatile("fence.proxy.alias;\n\tmultimem.st.release.sys.global.b64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+  unsigned long long r;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
   uint32_t r;
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");

@@ -17,6 +17,7 @@ uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, 
 // Whether a launch whose largest encode stream has n_chunks table chunks builds its tables with
 // the k_hist + k_norm launches (true) or with T items inside k_fused (false); UZIP_TABLE_KERNELS
 // overrides (A/B of the single-kernel table build).
+constexpr uint64_t kTableKernelChunks = 16;  // >= 128 MiB of 2-byte input per stream
 bool table_kernels(uint64_t n_chunks);
 
 }  // namespace uzip
