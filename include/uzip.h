@@ -203,7 +203,12 @@ UZIP_API uzip_status_t uzip_recv(void *buf, size_t count, uzip_dtype_t dtype, in
  *  allgather:      recvbuf[r*sendcount + i] = sendbuf_r[i]; one stream per rank sent to all peers
  *  reduce_scatter: recvbuf_r[i] = R(sendbuf_0[r*recvcount+i], ..., sendbuf_{N-1}[...]) with the
  *                  fixed-order fp32 fold R (R11); the own shard is never compressed
- *  allreduce:      two-shot = reduce_scatter + allgather of the reduced shards (count % nranks == 0)
+ *  allreduce:      two-shot = reduce_scatter + allgather of the reduced shards, any count: N shards of
+ *                  ceil(count/N) elements rounded up to 16 bytes (the last ones shorter or empty);
+ *                  compressed rounds run both phases in ONE launch, each reduced tile re-encoded from
+ *                  registers into the allgather stream (a9; its chunk tables sampled from each
+ *                  chunk's first tile, R26)
+ *  (reduce_scatter needs recvcount * element bytes % 16 == 0: 16-byte aligned shards, R21)
  * In place: allreduce sendbuf == recvbuf; allgather sendbuf == recvbuf + rank*sendcount;
  * reduce_scatter recvbuf == sendbuf + rank*recvcount. */
 UZIP_API uzip_status_t uzip_allgather(const void *sendbuf, void *recvbuf, size_t sendcount, uzip_dtype_t dtype,

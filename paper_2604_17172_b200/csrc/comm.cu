@@ -316,6 +316,18 @@ bool needs_coscheduling(const Plan &p) {
 uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
   if (c->share > 1 && serialized_env() && needs_coscheduling(p)) return UZIP_ERR_COMM;  // fail fast, no hang
   plan_flags(p);
+  static const bool dbg = getenv("UZIP_DEBUG_PLAN") != nullptr;
+  if (dbg) {
+    fprintf(stderr, "[rank %d] launch ne=%d nd=%d ag=%d:", c->rank, p.ne, p.nd_jobs, p.ag_job);
+    for (int j = 0; j < p.ne + (p.ag_job >= 0 ? 1 : 0); ++j)
+      fprintf(stderr, " E%d(raw%u n=%llu tiles=%llu ep=%u)", j, p.e[j].raw,
+              (unsigned long long)(p.e[j].raw ? p.e[j].raw_bytes : p.e[j].g.n), (unsigned long long)p.e[j].ntiles,
+              p.e[j].epoch[0]);
+    for (int j = 0; j < p.nd_jobs; ++j)
+      fprintf(stderr, " D%d(raw%u nsrc=%u me=%d tiles=%llu ep0=%u ep1=%u)", j, p.d[j].raw, p.d[j].nsrc, p.d[j].me,
+              (unsigned long long)p.d[j].ntiles, p.d[j].epoch[0], p.d[j].epoch[1]);
+    fprintf(stderr, "\n");
+  }
   for (int j = 0; j < p.ne; ++j) p.n_e_items += p.e[j].ntiles;
   for (int j = 0; j < p.nd_jobs; ++j) p.n_d_items += items_of(p.d[j]);
   p.n_c_items = p.has_copy ? p.c.ntiles : 0;
@@ -655,76 +667,89 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
   if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
   if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
   if (count == 0) return UZIP_OK;
-  const int N = c->nranks;
-  if (count % (size_t)N != 0) return UZIP_ERR_INVALID_ARG;
+  const int N = c->nranks, me = c->rank, dt = (int)dtype;
   if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
-  const uint32_t eb = elem_bytes((int)dtype);
-  const uint64_t shard = count / N;
-  if ((shard * eb) % 16 != 0 && N > 1) return UZIP_ERR_INVALID_ARG;  // shards stay 16-byte aligned
-  // Two-shot: reduce-scatter into my shard of recvbuf, then
-  // allgather of the reduced shards, each phase compressing once (R12).  The
-  // threshold applies to the user message (R10) in both phases.
-  const uint64_t saved = c->cfg.min_compress_bytes;
-  const bool comp = compress_message(c, count * eb);
-  static const bool fused = !(getenv("UZIP_AR_FUSED") && atoi(getenv("UZIP_AR_FUSED")) == 0);
-  if (comp && N > 1 && fused && !c->cfg.codec.global_table) {
-    // One pass per round (a9, R26): one launch holds the reduce-scatter streams (E items), the reduce
-    // items -- which round each reduced tile and code it straight into the allgather stream to the
-    // N-1 peers (no HBM round trip, no second table pass) -- and the decoders of the peers'
-    // allgather streams.  Its per-chunk tables are sampled from each chunk's first tile.
-    const int dt = (int)dtype, me = c->rank;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (uzip_status_t s2 = begin_call(c, 2ull * (N - 1) * shard * eb, true, st)) return s2;
-    if (uzip_status_t s2 = ensure_acc(c)) return s2;
-    const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
-    uint8_t *out = static_cast<uint8_t *>(recvbuf);
-    const uint64_t per = round_elems(c, dt, true, shard, nullptr);
-    const std::vector<int> peers = peers_from(c);
-    std::vector<int> all;
-    for (int r = 0; r < N; ++r) all.push_back(r);
-    for (uint64_t o = 0; o < shard; o += per) {
-      const uint64_t n = std::min<uint64_t>(per, shard - o);
-      Plan p;
-      base_plan(c, p, dt);
-      int j = 0;
-      for (int d : peers) {  // shard d of my input -> its owner (reduce-scatter streams)
-        enc_job(c, p, j, dt, in + ((uint64_t)d * shard + o) * eb, n, true, {d});
-        ++j;
-      }
-      uint8_t *mine = out + ((uint64_t)me * shard + o) * eb;
-      dec_job(c, p, 0, dt, n, true, all, me, in + ((uint64_t)me * shard + o) * eb, mine);
+  const uint32_t eb = elem_bytes(dt);
+  // Two-shot over N shards of `shard` elements (the last ones shorter or empty when
+  // count % N != 0): shards start on 16-byte boundaries, so any count works, as with NCCL (R21).
+  const uint64_t align = 16 / eb;
+  const uint64_t shard = ((count + N - 1) / N + align - 1) / align * align;
+  auto len_of = [&](int j) -> uint64_t {
+    const uint64_t lo = std::min<uint64_t>(count, (uint64_t)j * shard);
+    return std::min<uint64_t>(shard, count - lo);
+  };
+  const bool comp = compress_message(c, count * eb);  // the user message decides both phases (R10)
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t *in = static_cast<const uint8_t *>(sendbuf);
+  uint8_t *out = static_cast<uint8_t *>(recvbuf);
+  if (N == 1) {
+    if (uzip_status_t s2 = begin_call(c, 0, comp, st)) return s2;
+    if (in != out && cudaMemcpyAsync(out, in, count * eb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return UZIP_ERR_CUDA;
+    return UZIP_OK;
+  }
+  static const bool fused_env = !(getenv("UZIP_AR_FUSED") && atoi(getenv("UZIP_AR_FUSED")) == 0);
+  // One pass per round (a9, R26): one launch holds the reduce-scatter streams (E items), the reduce
+  // items -- which round each reduced tile and code it straight into the allgather stream to the N-1
+  // peers (no HBM round trip, no second table pass) -- and the decoders of the peers' allgather
+  // streams, whose per-chunk tables are sampled from each chunk's first tile.  Below the threshold,
+  // or with one global table (it needs every reduced symbol first), a round is two launches:
+  // reduce-scatter, then allgather of the reduced shard (re-read from recvbuf).
+  const bool fused = comp && fused_env && !c->cfg.codec.global_table;
+  uint64_t egress = 0;
+  for (int d = 0; d < N; ++d)
+    if (d != me) egress += (len_of(d) + len_of(me)) * eb;
+  if (uzip_status_t s2 = begin_call(c, egress, comp, st)) return s2;
+  if (uzip_status_t s2 = ensure_acc(c)) return s2;
+  const uint64_t per = round_elems(c, dt, comp, shard, nullptr);
+  const std::vector<int> peers = peers_from(c);
+  std::vector<int> all;
+  for (int r = 0; r < N; ++r) all.push_back(r);
+  auto part = [&](int j, uint64_t o) -> uint64_t { const uint64_t L = len_of(j); return L > o ? std::min(per, L - o) : 0; };
+  for (uint64_t o = 0; o < shard; o += per) {
+    const uint64_t nme = part(me, o);
+    uint8_t *mine = out + ((uint64_t)me * shard + o) * eb;
+    Plan p;
+    base_plan(c, p, dt);
+    int j = 0;
+    for (int d : peers)  // shard d of my input -> its owner (reduce-scatter streams)
+      if (const uint64_t n = part(d, o)) enc_job(c, p, j++, dt, in + ((uint64_t)d * shard + o) * eb, n, comp, {d});
+    if (nme) {
+      dec_job(c, p, 0, dt, nme, comp, all, me, in + ((uint64_t)me * shard + o) * eb, mine);
       p.d[0].op = (uint32_t)op;
+    }
+    if (fused && nme) {
       // single tiles per reduce item: the re-encoded tiles finish their look-back in tile order, so
       // runs of consecutive tiles per CTA would chain the CTAs (measured 4x slower at N = 2)
       p.d[0].run = 1;
-      // the allgather stream of my reduced shard: e[N-1], no E items of its own (p.ne stays N-1)
+      // the allgather stream of my reduced shard: e[ne], no E items of its own (p.ne unchanged)
       const int ne = p.ne;
-      enc_job(c, p, ne, dt, mine, n, true, peers);
+      enc_job(c, p, ne, dt, mine, nme, true, peers);
       p.ne = ne;
       p.ag_job = ne;
       uzip_codec_params_t cp = c->cfg.codec;
-      resolve_geom(dt, n, &cp, &p.e[ne].g);
+      resolve_geom(dt, nme, &cp, &p.e[ne].g);
       cp.sample_symbols = kTileBlocks * p.e[ne].g.B;  // R26: the chunk's first tile is its sample
-      resolve_geom(dt, n, &cp, &p.e[ne].g);
-      j = 1;
-      for (int s : peers) {  // the peers' reduced shards
-        dec_job(c, p, j, dt, n, true, {s}, -1, nullptr, out + ((uint64_t)s * shard + o) * eb);
-        ++j;
-      }
-      if (uzip_status_t s2 = launch(c, p, true, st)) return s2;
+      resolve_geom(dt, nme, &cp, &p.e[ne].g);
     }
-    return UZIP_OK;
+    if (fused) {
+      int k = nme ? 1 : 0;
+      for (int s : peers)  // the peers' reduced shards
+        if (const uint64_t n = part(s, o)) dec_job(c, p, k++, dt, n, true, {s}, -1, nullptr, out + ((uint64_t)s * shard + o) * eb);
+    }
+    if (p.ne || p.nd_jobs)
+      if (uzip_status_t s2 = launch(c, p, comp, st)) return s2;
+    if (fused) continue;
+    Plan q;  // allgather of the reduced shard (two-launch rounds)
+    base_plan(c, q, dt);
+    if (nme) enc_job(c, q, 0, dt, mine, nme, comp, peers);
+    int k = 0;
+    for (int s : peers)
+      if (const uint64_t n = part(s, o)) dec_job(c, q, k++, dt, n, comp, {s}, -1, nullptr, out + ((uint64_t)s * shard + o) * eb);
+    if (q.ne || q.nd_jobs)
+      if (uzip_status_t s2 = launch(c, q, comp, st)) return s2;
   }
-  uzip_status_t s = begin_call(c, 0, comp, (cudaStream_t)stream);
-  if (s != UZIP_OK) return s;
-  c->cfg.min_compress_bytes = comp ? 0 : ~0ull;
-  c->nested = 1;
-  uint8_t *mine = static_cast<uint8_t *>(recvbuf) + (uint64_t)c->rank * shard * eb;
-  s = uzip_reduce_scatter(sendbuf, mine, shard, dtype, op, c, stream);
-  if (s == UZIP_OK && N > 1) s = uzip_allgather(mine, recvbuf, shard, dtype, c, stream);
-  c->nested = 0;
-  c->cfg.min_compress_bytes = saved;
-  return s;
+  return UZIP_OK;
 }
 
 uzip_status_t uzip_alltoall(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype, uzip_comm_t c,

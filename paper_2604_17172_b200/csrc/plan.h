@@ -99,6 +99,7 @@ struct Plan {
   DecJob d[kMaxRanks];
   CopyJob c;
   uint64_t n_t_items, n_e_items, n_c_items, n_d_items;
+  uint64_t e_tmin;                          // fewest tiles of any encode job (E items are tile-major)
   uint32_t *ticket;                         // self-resetting ticket + exit counter (2 words)
   uint32_t *epoch;                          // launch epoch of this workspace (24 bits): read by every CTA at
                                             // start, advanced by the last CTA out; tags the look-back words
@@ -189,12 +190,40 @@ __host__ __device__ inline void t_item_at(const EncJob &J, uint64_t k, uint64_t 
   }
 }
 
+// E item `it` -> (job, tile).  Tile-major over the encode jobs (every destination receives tile t of
+// its stream at about the same time); jobs may have different tile counts (uneven allreduce shards):
+// below the smallest count the map is it % ne / it / ne, above it the jobs that still have tile t
+// take turns in job order.
+__host__ __device__ inline void e_item_at(const Plan &P, uint64_t it, int &job, uint64_t &tile) {
+  const uint64_t ne = (uint64_t)P.ne;
+  if (it < P.e_tmin * ne) {
+    job = (int)(it % ne);
+    tile = it / ne;
+    return;
+  }
+  uint64_t r = it - P.e_tmin * ne;
+  for (uint64_t t = P.e_tmin;; ++t) {
+    for (int j = 0; j < P.ne; ++j)
+      if (P.e[j].ntiles > t) {
+        if (r == 0) {
+          job = j;
+          tile = t;
+          return;
+        }
+        --r;
+      }
+  }
+}
+
 // Host: derive EncJob::has_flags of every encode job of a plan (call before the launch).
 inline void plan_flags(Plan &p) {
   for (int j = 0; j < kMaxRanks; ++j) {
     p.e[j].has_flags = 0;
     for (uint32_t d = 0; d < p.e[j].nd; ++d) p.e[j].has_flags |= p.e[j].flag[d] != nullptr;
   }
+  p.e_tmin = ~0ull;
+  for (int j = 0; j < p.ne; ++j) p.e_tmin = p.e[j].ntiles < p.e_tmin ? p.e[j].ntiles : p.e_tmin;
+  if (p.ne == 0) p.e_tmin = 0;
 }
 
 static_assert(sizeof(Plan) <= 30000, "kernel parameter space");
