@@ -456,6 +456,9 @@ struct FusedShared {
   unsigned long long red64[kWarps];
   uint32_t epoch;  // this launch's epoch (Plan::epoch)
   uint32_t is_last;
+  // abort words of the other wait sites: each site has its own, so a warp still reading one site's
+  // outcome never sees the next site's write (compute-sanitizer racecheck)
+  uint32_t ab_credit, ab_table;
 };
 
 // ---------------------------------------------------------------- E item
@@ -807,10 +810,10 @@ static __device__ bool credit_gate(const Plan &P, const EncJob &J, int jidx, uin
     if (P.credit_ready) ok = ld_volatile_u32(P.err) == 0;  // k_credit waited (or failed)
     else
       for (uint32_t d = 0; d < J.nd && ok; ++d) ok = wait_credit(P, J.credit[d], J.epoch[d]);
-    S.abort = ok ? 0u : 1u;
+    S.ab_credit = ok ? 0u : 1u;
   }
   __syncthreads();
-  if (S.abort) return false;
+  if (S.ab_credit) return false;
   credit_done |= 1u << jidx;
   return true;
 }
@@ -999,10 +1002,10 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
     if (!P.tables_ready) {
       if (tid == 0) {  // the chunk's table: published by its last T item (a smaller ticket)
         unsigned long long seen = 0;
-        S.abort = wait_u64(P, J.tflag + c, kCtlTag | (S.epoch + 1u), seen) ? 0u : 1u;
+        S.ab_table = wait_u64(P, J.tflag + c, kCtlTag | (S.epoch + 1u), seen) ? 0u : 1u;
       }
       __syncthreads();
-      if (S.abort) return;
+      if (S.ab_table) return;
     }
     tab[tid] = J.enc[c * 256 + tid];  // after the acquire (gpu scope): plain loads see the T item's stores
     enc_key = key;
@@ -1118,10 +1121,10 @@ static __device__ void forward_tile(const Plan &P, const DecJob &J, uint64_t t, 
       if (P.credit_ready) ok = ld_volatile_u32(P.err) == 0;
       else
         for (uint32_t d = 0; d < J.nfwd && ok; ++d) ok = wait_credit(P, J.fcredit[d], J.fepoch[d]);
-      S.abort = ok ? 0u : 1u;
+      S.ab_credit = ok ? 0u : 1u;
     }
     __syncthreads();
-    if (S.abort) return;
+    if (S.ab_credit) return;
     fwd_done |= 1u << jidx;
   }
   const unsigned long long tile_off = S.src_off[0];
@@ -1463,10 +1466,10 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     } else if (ga.n_blocks && key != enc_key) {
       if (tid == 0) {  // the chunk's first tile (a smaller ticket) publishes the table
         unsigned long long v = 0;
-        S.abort = wait_u64(P, tabflag + ca, kCtlTag | (S.epoch + 1u), v) ? 0u : 1u;
+        S.ab_table = wait_u64(P, tabflag + ca, kCtlTag | (S.epoch + 1u), v) ? 0u : 1u;
       }
       __syncthreads();
-      if (S.abort) return;
+      if (S.ab_table) return;
       tab[tid] = ld_cg_v4(A.enc + ca * 256 + tid);
       enc_key = key;
       __syncthreads();
