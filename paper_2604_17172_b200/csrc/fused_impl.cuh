@@ -659,11 +659,12 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
         if (p && idx + 1 < kCap)
           for (uint32_t d = 0; d < J.nd; ++d)
             *reinterpret_cast<uint16_t *>(J.dst[d] + g.off_pay + off + 128 + 2 * idx) = (uint16_t)x;
+        x = p ? (x >> 16) : x;
       } else {
         buf16[didx] = (uint16_t)dw;
         dw = x, didx = p ? idx : spare;
+        x = p ? (x >> 16) : x;  // (an inline-PTX predicated shift instead of the select: no change, 0.704 ms)
       }
-      x = p ? (x >> 16) : x;
       wp += __popc(m);
       const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
       x = x + e.z + q * e.w;
