@@ -259,6 +259,13 @@ UZIP_API uzip_status_t uzip_comm_error_detail(uzip_comm_t comm, uint32_t *out16)
  * rank `src`'s rounds land on this rank into host memory (sync).  Round q of
  * the ordered pair (src, this rank) lands in slot q % 2 as one UZB1 stream
  * (the oracle's wire stream). */
+/* Tile trace (overlap evidence without a timeline profiler): with UZIP_TRACE=1 in the
+ * environment at communicator init, every fused launch appends events of two u64 -- kind:4 | job:4 |
+ * tile:56, then %globaltimer ns -- kinds 1 = encode tile started, 2 = its flag released, 3 = decode tile
+ * acquired, 4 = decode tile done.  Copies up to max_events of them to `host` (2 x u64 each), sets
+ * *n_events and clears the buffer (synchronizes the device).  Off: *n_events = 0. */
+UZIP_API uzip_status_t uzip_comm_trace(uzip_comm_t comm, unsigned long long *host, size_t max_events,
+                                       size_t *n_events);
 UZIP_API uzip_status_t uzip_comm_read_staging(uzip_comm_t comm, int src, int slot, void *host, size_t bytes);
 
 UZIP_API const char *uzip_status_string(uzip_status_t s);

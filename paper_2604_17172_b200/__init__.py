@@ -40,7 +40,7 @@ EXPORTED = [
     "uzip_reduce_scatter", "uzip_allreduce", "uzip_comm_get_async_error", "uzip_get_stats",
     "uzip_status_string", "uzip_version", "uzip_comm_read_staging", "uzip_broadcast",
     "uzip_alltoall", "uzip_comm_error_detail", "uzip_staged_workspace_bytes", "uzip_compress_staged",
-    "uzip_nvls_supported", "uzip_nvls_selftest",
+    "uzip_nvls_supported", "uzip_nvls_selftest", "uzip_comm_trace",
 ]
 
 
@@ -115,6 +115,8 @@ def lib() -> ctypes.CDLL:
                 l.uzip_compress_staged.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp, vp, vp]
                 l.uzip_nvls_supported.argtypes = [i32, ctypes.POINTER(i32)]
                 l.uzip_nvls_selftest.argtypes = [i32, sz]
+            if hasattr(l, "uzip_comm_trace"):
+                l.uzip_comm_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
             l.uzip_status_string.argtypes = [i32]
             l.uzip_status_string.restype = ctypes.c_char_p
             l.uzip_version.restype = ctypes.c_char_p
@@ -408,6 +410,18 @@ class Comm:
         buf = (ctypes.c_uint32 * 16)()
         _check(lib().uzip_comm_error_detail(self.h, buf), "uzip_comm_error_detail")
         return list(buf)
+
+    def trace(self, max_events: int = 1 << 20):
+        """Tile trace events (UZIP_TRACE=1 at init): numpy array of (kind, job, tile, t_ns) rows."""
+        import numpy as np
+        buf = np.zeros(2 * max_events, np.uint64)
+        n = ctypes.c_size_t(0)
+        _check(lib().uzip_comm_trace(self.h, buf.ctypes.data, max_events, ctypes.byref(n)), "uzip_comm_trace")
+        ev = buf[: 2 * n.value].reshape(-1, 2)
+        kind = (ev[:, 0] >> np.uint64(60)).astype(np.int64)
+        job = ((ev[:, 0] >> np.uint64(56)) & np.uint64(15)).astype(np.int64)
+        tile = (ev[:, 0] & np.uint64((1 << 56) - 1)).astype(np.int64)
+        return np.stack([kind, job, tile, ev[:, 1].astype(np.int64)], axis=1) if n.value else np.zeros((0, 4), np.int64)
 
     def stats(self) -> dict:
         s = Stats()

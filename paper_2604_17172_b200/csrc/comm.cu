@@ -67,6 +67,9 @@ struct uzip_comm {
   uint32_t call_rounds;            // fused launches issued by the current call
   uint32_t share;                  // ranks (incl. this one) whose kernels run on this same GPU
   float *acc;                      // reduce accumulators (allocated by the first reduce call)
+  unsigned long long *trace;       // tile trace events (UZIP_TRACE=1), 2 x u64 each
+  uint32_t *trace_n;
+  uint32_t trace_cap;
 };
 
 namespace {
@@ -113,6 +116,12 @@ uzip_status_t alloc_local(uzip_comm *c) {
   if (cudaMemset(c->ws, 0, c->ws_bytes) != cudaSuccess) return UZIP_ERR_CUDA;
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return UZIP_ERR_CUDA;
   if (preload_kernels() != cudaSuccess) return UZIP_ERR_CUDA;
+  if (getenv("UZIP_TRACE") && atoi(getenv("UZIP_TRACE")) != 0) {  // tile trace (overlap evidence)
+    c->trace_cap = 1u << 20;
+    if (cudaMalloc(&c->trace, 16ull * c->trace_cap + 16) != cudaSuccess) return UZIP_ERR_CUDA;
+    c->trace_n = reinterpret_cast<uint32_t *>(c->trace + 2ull * c->trace_cap);
+    if (cudaMemset(c->trace_n, 0, 16) != cudaSuccess) return UZIP_ERR_CUDA;
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return UZIP_ERR_CUDA;
   return UZIP_OK;
 }
@@ -137,6 +146,7 @@ void free_comm(uzip_comm *c) {
   if (c->region) cudaFree(c->region);
   if (c->ws) cudaFree(c->ws);
   if (c->acc) cudaFree(c->acc);
+  if (c->trace) cudaFree(c->trace);
   if (c->side) cudaStreamDestroy(c->side);
   c->magic = 0;
   delete c;
@@ -197,6 +207,9 @@ void base_plan(uzip_comm *c, Plan &p, int dt) {
   p.dtype = dt;
   p.ticket = ws_ticket(c);
   p.epoch = reinterpret_cast<uint32_t *>(c->ws + 8);
+  p.trace = c->trace;
+  p.trace_n = c->trace_n;
+  p.trace_cap = c->trace_cap;
   p.err = reinterpret_cast<uint32_t *>(c->region);
   p.acc = c->acc;
   p.timeout_ns = (uint64_t)c->cfg.poll_timeout_ms * 1000000ull;
@@ -908,6 +921,21 @@ uzip_status_t uzip_comm_read_staging(uzip_comm_t c, int src, int slot, void *hos
   if (cudaMemcpyAsync(host, c->region + c->L.stage(src, slot), bytes, cudaMemcpyDeviceToHost, c->side) != cudaSuccess)
     return UZIP_ERR_CUDA;
   return cudaStreamSynchronize(c->side) == cudaSuccess ? UZIP_OK : UZIP_ERR_CUDA;
+}
+
+uzip_status_t uzip_comm_trace(uzip_comm_t c, unsigned long long *host, size_t max_events, size_t *n_events) {
+  if (!valid(c) || !n_events) return UZIP_ERR_INVALID_ARG;
+  *n_events = 0;
+  if (!c->trace) return UZIP_OK;  // tracing off (UZIP_TRACE unset at init)
+  cudaSetDevice(c->device);
+  if (cudaDeviceSynchronize() != cudaSuccess) return UZIP_ERR_CUDA;
+  uint32_t n = 0;
+  if (cudaMemcpy(&n, c->trace_n, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return UZIP_ERR_CUDA;
+  n = std::min<uint32_t>(n, c->trace_cap);
+  const size_t k = std::min<size_t>(n, max_events);
+  if (k && host && cudaMemcpy(host, c->trace, 16 * k, cudaMemcpyDeviceToHost) != cudaSuccess) return UZIP_ERR_CUDA;
+  *n_events = k;
+  return cudaMemset(c->trace_n, 0, 4) == cudaSuccess ? UZIP_OK : UZIP_ERR_CUDA;
 }
 
 uzip_status_t uzip_get_stats(uzip_comm_t c, uzip_stats_t *out) {

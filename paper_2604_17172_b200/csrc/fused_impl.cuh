@@ -244,6 +244,17 @@ __device__ __forceinline__ void raise_err_at(const Plan &P, uint32_t code, uint3
   }
 }
 
+// Tile trace (Plan::trace): one event, thread-level.
+__device__ __forceinline__ void trace_ev(const Plan &P, uint32_t kind, uint32_t job, uint64_t tile) {
+  if (!P.trace) return;
+  const uint32_t i = atomicAdd(P.trace_n, 1u);
+  if (i < P.trace_cap) {
+    P.trace[2ull * i] = ((unsigned long long)kind << 60) | ((unsigned long long)(job & 15u) << 56) |
+                        (tile & ((1ull << 56) - 1));
+    P.trace[2ull * i + 1] = globaltimer_ns();
+  }
+}
+
 // Debug stress (UZIP_STRESS=seed): a pseudo-random pause of up to ~16 us at the protocol's hand-off
 // points, so the loopback tests exercise late flags, early credits and reordered tiles.
 __device__ __forceinline__ void stress_pause(const Plan &P, uint64_t salt) {
@@ -706,7 +717,8 @@ struct EncPending {
 template <int DT, int B>
 static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint8_t *ring, EncPending &pd) {
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  const EncJob &J = P.e[pd.job];
+  const int jidx = pd.job;
+  const EncJob &J = P.e[jidx];
   const StreamGeom &g = J.g;
   const uint64_t t = pd.t;
   pd.job = -1;
@@ -754,6 +766,7 @@ static __device__ void resolve_pending(const Plan &P, FusedShared &S, const uint
             stress_pause(P, t * 7 + d);
             st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
           }
+          trace_ev(P, kTrEFlag, (uint32_t)jidx, t);
         }
       }
     }
@@ -949,6 +962,7 @@ static __device__ void code_tile(const Plan &P, const EncJob &J, int jidx, uint6
             stress_pause(P, t * 7 + d);
             st_release_sys_u64(J.flag[d] + t, ((unsigned long long)J.epoch[d] << 32) | off16);
           }
+        trace_ev(P, kTrEFlag, (uint32_t)jidx, t);
       }
     }
   }
@@ -965,6 +979,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   const int tid = threadIdx.x, warp = warp_id();
   (void)next_it;  // an L2 prefetch of the next tile by warp 0 was measured slower (r1: 0.784 vs 0.754 ms/GiB)
   if (!credit_gate(P, J, jidx, credit_done, S)) return;
+  if (tid == 0) trace_ev(P, kTrEStart, (uint32_t)jidx, t);
   const bool flags = J.has_flags != 0;
 
   if (J.raw) {  // ---- below the threshold: raw 64 KiB tiles (a11)
@@ -987,6 +1002,7 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
           stress_pause(P, t * 11 + d);
           st_release_sys_u64(J.flag[d] + t, (unsigned long long)J.epoch[d] << 32);
         }
+      trace_ev(P, kTrEFlag, (uint32_t)jidx, t);
     }
     return;
   }
@@ -1032,8 +1048,9 @@ static __device__ void copy_item(const CopyJob &Cj, uint64_t t) {
 }
 
 // Completion of one D item: the last tile of the job releases the sources' slots.
-static __device__ void dec_done(const DecJob &J) {
+static __device__ void dec_done(const Plan &P, const DecJob &J, int jidx, uint64_t t) {
   if (threadIdx.x != 0) return;
+  trace_ev(P, kTrDDone, (uint32_t)jidx, t);
   __threadfence();
   const uint32_t old = atomicAdd(J.done, 1u);
   if (old == (uint32_t)J.ntiles - 1) {
@@ -1180,7 +1197,10 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
   const uint64_t c = g.n_blocks ? chunk_of(g, b0) : 0;
   const uint64_t key = (1ull << 63) | ((uint64_t)jidx << 48) | c;
   const bool need_table = key != dec_key;
-  if (tid == 0) acquire_tile(P, J, 0, t, need_table, S);
+  if (tid == 0) {
+    acquire_tile(P, J, 0, t, need_table, S);
+    trace_ev(P, kTrDAcq, (uint32_t)jidx, t);
+  }
   __syncthreads();
   if (S.abort) return;
   const uint8_t *stream = J.src[0];
@@ -1192,7 +1212,7 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
       st_any16(J.out + o0 + 16 * i, ld_cg_v4(stream + o0 + 16 * i));
     for (uint64_t i = nv * 16 + tid; i < len; i += 256) J.out[o0 + i] = stream[o0 + i];
     __syncthreads();
-    dec_done(J);
+    dec_done(P, J, jidx, t);
     return;
   }
   if (J.nfwd) {  // relay first: the next hops receive the tile before it is decoded here
@@ -1233,7 +1253,7 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
     for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
   }
   __syncthreads();
-  dec_done(J);
+  dec_done(P, J, jidx, t);
 }
 
 // The warp's fp32 accumulator lives in global memory (P.acc, B floats per
@@ -1313,7 +1333,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
       else *reinterpret_cast<uint16_t *>(J.out + o0 + i * eb) = (uint16_t)r;
     }
     __syncthreads();
-    dec_done(J);
+    dec_done(P, J, jidx, t);
     return;
   }
 
@@ -1478,7 +1498,7 @@ static __device__ void red_item(const Plan &P, const DecJob &J, int jidx, uint64
     code_tile<DT, B, true>(P, A, P.ag_job, t, smem, S, ring, P.ring_bytes, pd, A.in);
   }
   __syncthreads();
-  dec_done(J);
+  dec_done(P, J, jidx, t);
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -1633,7 +1653,14 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   // Ranks sharing this GPU (loopback): a launch whose decode items spin on a
   // peer's flags may hold at most 1/share of the slots, so the peer's kernels
   // (the producers it waits for) always find an SM.
-  if (p.share > 1 && p.n_d_items > 0 && grid > sm_count() * occ / (int)p.share)
+#ifndef UZIP_SHARE_ENC_CAP
+#define UZIP_SHARE_ENC_CAP 0
+#endif
+  // Encode-only launches stay uncapped by default: capping them to 1/share did not let a receiver
+  // launched after its sender start any earlier on the shared GPU (tile trace: 0 % of its tiles
+  // decoded before the sender's last flag either way) and slowed the sender (loopback 1 GiB P2P 2.03-2.15
+  // vs 1.98 ms).  A receiver launched first overlaps (98 % of its tiles decoded while the sender runs).
+  if (p.share > 1 && (p.n_d_items > 0 || UZIP_SHARE_ENC_CAP) && grid > sm_count() * occ / (int)p.share)
     grid = sm_count() * occ / (int)p.share > 0 ? sm_count() * occ / (int)p.share : 1;
   if ((uint64_t)grid > items) grid = (int)(items ? items : 1);
   kern<<<grid, 256, smem, st>>>(p);

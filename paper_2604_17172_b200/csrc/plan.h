@@ -120,7 +120,16 @@ struct Plan {
   int32_t ag_job;                           // -1: none
   uint32_t tables_ready;                    // 1: k_hist + k_norm built every encode table before this
                                             // launch (stream order), E items skip the table flag wait
+  // optional tile trace (UZIP_TRACE=1, communicators only): events of 2 x u64 -- kind:4 | job:4 | tile:56,
+  // %globaltimer ns -- appended through *trace_n (uzip_comm_trace); null when off
+  unsigned long long *trace;
+  uint32_t *trace_n;
+  uint32_t trace_cap;
 };
+
+// Tile trace event kinds (overlap evidence: E items publish tiles while D items of the same round,
+// on the peer, decode earlier ones).
+enum TraceKind : uint32_t { kTrEStart = 1, kTrEFlag = 2, kTrDAcq = 3, kTrDDone = 4 };
 
 // Slot credits one launch needs (a12), waited for by k_credit -- one thread --
 // before the fused kernel starts, so its CTAs never hold SM slots while the

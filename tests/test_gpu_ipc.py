@@ -100,3 +100,19 @@ def test_table_kernel_path_equals_oracle():
            "stream_bytes_equal_oracle or stream_params or wire_stream or allreduce_fused or tie"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_tile_trace_shows_overlap():
+    """The tile trace (UZIP_TRACE=1) of a loopback split-send P2P: the receiver decodes tiles while the
+    sender is still encoding later ones, and the one-pass allreduce releases allgather tiles while later
+    tiles of its shard are still being reduced (overlap evidence)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+    env = dict(os.environ, UZIP_TRACE="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "overlap_trace.py"), "--mib", "64"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["tiles"] > 100 and res["receiver_tiles_done_before_sender_finished"] > 0.25
+    assert res["allreduce_one_pass"]["ag_tiles_released_before_last_reduced_tile"] > 0.25
