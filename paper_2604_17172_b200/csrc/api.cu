@@ -79,6 +79,7 @@ uzip_status_t uzip_workspace_init(void *ws, size_t ws_bytes, void *stream) {
 uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, void *out, size_t out_capacity,
                             uint64_t *d_out_bytes, void *ws, size_t ws_bytes, const uzip_codec_params_t *params,
                             void *stream) {
+  NvtxRange nvtx_range("uzip_compress");
   StreamGeom g;
   uzip_status_t st = resolve_geom((int)dtype, count, params, &g);
   if (st != UZIP_OK) return st;
@@ -126,6 +127,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
 
 uzip_status_t uzip_decompress(const void *in, size_t in_bytes, void *out, size_t count, uzip_dtype_t dtype,
                               int32_t *d_status, void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_range("uzip_decompress");
   if ((int)dtype < 0 || (int)dtype >= kNumDtypes) return UZIP_ERR_UNSUPPORTED_DTYPE;
   if (!in || !ws || !d_status || !aligned16(in) || !aligned16(ws)) return UZIP_ERR_INVALID_ARG;
   if (count > 0 && (!out || !aligned16(out))) return UZIP_ERR_INVALID_ARG;

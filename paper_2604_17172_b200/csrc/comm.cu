@@ -441,6 +441,7 @@ extern "C" {
 
 uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_device, uzip_allgather_fn bootstrap,
                              void *ctx, const uzip_config_t *cfg) {
+  NvtxRange nvtx_range("uzip_comm_init");
   if (!comm || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !bootstrap)
     return UZIP_ERR_INVALID_ARG;
   *comm = nullptr;
@@ -504,6 +505,7 @@ uzip_status_t uzip_comm_init(uzip_comm_t *comm, int nranks, int rank, int cuda_d
 }
 
 uzip_status_t uzip_comm_init_all(uzip_comm_t *comms, int nranks, const int *devices, const uzip_config_t *cfg) {
+  NvtxRange nvtx_range("uzip_comm_init_all");
   if (!comms || !devices || nranks < 1 || nranks > kMaxRanks) return UZIP_ERR_INVALID_ARG;
   std::vector<uzip_comm *> cs(nranks, nullptr);
   for (int r = 0; r < nranks; ++r) {
@@ -545,6 +547,7 @@ uzip_status_t uzip_comm_destroy(uzip_comm_t comm) {
 }
 
 uzip_status_t uzip_send(const void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t c, void *stream) {
+  NvtxRange nvtx_range("uzip_send");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_dtype(dtype)) return s;
   if (peer < 0 || peer >= c->nranks || peer == c->rank) return UZIP_ERR_INVALID_ARG;
@@ -567,6 +570,7 @@ uzip_status_t uzip_send(const void *buf, size_t count, uzip_dtype_t dtype, int p
 }
 
 uzip_status_t uzip_recv(void *buf, size_t count, uzip_dtype_t dtype, int peer, uzip_comm_t c, void *stream) {
+  NvtxRange nvtx_range("uzip_recv");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_dtype(dtype)) return s;
   if (peer < 0 || peer >= c->nranks || peer == c->rank) return UZIP_ERR_INVALID_ARG;
@@ -590,6 +594,7 @@ uzip_status_t uzip_recv(void *buf, size_t count, uzip_dtype_t dtype, int peer, u
 
 uzip_status_t uzip_allgather(const void *sendbuf, void *recvbuf, size_t sendcount, uzip_dtype_t dtype,
                              uzip_comm_t c, void *stream) {
+  NvtxRange nvtx_range("uzip_allgather");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_dtype(dtype)) return s;
   if (sendcount == 0) return UZIP_OK;
@@ -630,6 +635,7 @@ uzip_status_t uzip_allgather(const void *sendbuf, void *recvbuf, size_t sendcoun
 
 uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t recvcount, uzip_dtype_t dtype,
                                   uzip_op_t op, uzip_comm_t c, void *stream) {
+  NvtxRange nvtx_range("uzip_reduce_scatter");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
   if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
@@ -676,6 +682,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
 
 uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype, uzip_op_t op,
                              uzip_comm_t c, void *stream) {
+  NvtxRange nvtx_range("uzip_allreduce");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
   if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
@@ -767,6 +774,7 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
 
 uzip_status_t uzip_alltoall(const void *sendbuf, void *recvbuf, size_t count, uzip_dtype_t dtype, uzip_comm_t c,
                             void *stream) {
+  NvtxRange nvtx_range("uzip_alltoall");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_dtype(dtype)) return s;
   if (count == 0) return UZIP_OK;
@@ -817,6 +825,7 @@ uzip_status_t uzip_alltoall(const void *sendbuf, void *recvbuf, size_t count, uz
 }
 
 uzip_status_t uzip_broadcast(void *buf, size_t count, uzip_dtype_t dtype, int root, uzip_comm_t c, void *stream) {
+  NvtxRange nvtx_range("uzip_broadcast");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
   if (uzip_status_t s = check_dtype(dtype)) return s;
   if (root < 0 || root >= c->nranks) return UZIP_ERR_INVALID_ARG;

@@ -5,7 +5,15 @@
 #include "../../include/uzip.h"
 #include "uzip_device.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges are free unless a profiler is attached
+
 namespace uzip {
+
+// NVTX range around one C-ABI call (host side: the enqueue, visible in nsys / ncu timelines).
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void *out, uint64_t n, void *ws,
                               int32_t *d_status, cudaStream_t st, int max_ctas);
