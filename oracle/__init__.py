@@ -73,6 +73,8 @@ def lib():
         l.uzo_normalize.argtypes = [vp, vp]
         l.uzo_encode_block.argtypes = [vp, u32, vp, vp, vp]
         l.uzo_encode_block.restype = u32
+        l.uzo_encode_block_l.argtypes = [vp, u32, vp, vp, vp, u32]
+        l.uzo_encode_block_l.restype = u32
         l.uzo_decode_block.argtypes = [vp, vp, u32, u32, vp, vp]
         l.uzo_decode_block.restype = i32
         l.uzo_compress_bound.argtypes = [sz, i32, ctypes.POINTER(Params)]
@@ -148,6 +150,18 @@ def encode_block(sym: np.ndarray, freq: np.ndarray):
     states = np.zeros(32, np.uint32)
     words = np.zeros(max(B, 1), np.uint16)
     K = lib().uzo_encode_block(_ptr(sym), B, _ptr(freq), _ptr(states), _ptr(words))
+    return states, words[:K].copy()
+
+
+def encode_block_l(sym: np.ndarray, freq: np.ndarray, lbits: int):
+    """encode_block with the state interval [2^lbits, 2^(lbits+16)) -- 15 is the format (R4), 16 the
+    survey prototype's interval (its g1 micro-vector pins the coder)."""
+    sym = np.ascontiguousarray(sym, dtype=np.uint8)
+    freq = np.ascontiguousarray(freq, dtype=np.uint16)
+    B = sym.size
+    states = np.zeros(32, np.uint32)
+    words = np.zeros(max(B, 1), np.uint16)
+    K = lib().uzo_encode_block_l(_ptr(sym), B, _ptr(freq), _ptr(states), _ptr(words), lbits)
     return states, words[:K].copy()
 
 

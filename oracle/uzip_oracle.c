@@ -174,10 +174,18 @@ static void cumulative(const uint16_t freq[256], uint32_t cdf[257]) {
  * within a round).  R4 in DESIGN.md. */
 uint32_t uzo_encode_block(const uint8_t *sym, uint32_t B, const uint16_t freq[256],
                           uint32_t states[32], uint16_t *words) {
+  return uzo_encode_block_l(sym, B, freq, states, words, UZO_STATE_LBITS);
+}
+
+/* The same coder for a state interval [2^lbits, 2^(lbits+16)) (lbits 15 or 16).  lbits = 15 is the
+ * stream format (R4); lbits = 16 is the interval of the survey's independent prototype, whose g1
+ * micro-vector then pins this function's arithmetic byte for byte. */
+uint32_t uzo_encode_block_l(const uint8_t *sym, uint32_t B, const uint16_t freq[256],
+                            uint32_t states[32], uint16_t *words, uint32_t lbits) {
   uint32_t cdf[257];
   cumulative(freq, cdf);
   uint32_t x[32];
-  for (uint32_t l = 0; l < UZO_LANES; ++l) x[l] = UZO_L;
+  for (uint32_t l = 0; l < UZO_LANES; ++l) x[l] = 1u << lbits;
   uint32_t K = 0;
   uint32_t R = B / UZO_LANES;
   for (uint32_t jj = R; jj > 0; --jj) {
@@ -185,7 +193,7 @@ uint32_t uzo_encode_block(const uint8_t *sym, uint32_t B, const uint16_t freq[25
     for (uint32_t l = 0; l < UZO_LANES; ++l) {
       uint32_t s = sym[j * UZO_LANES + l];
       uint32_t f = freq[s];
-      uint32_t x_max = f << (31u - UZO_PROB_BITS);
+      uint32_t x_max = f << (lbits + 16u - UZO_PROB_BITS);  /* (L >> P) << 16, times f */
       if (x[l] >= x_max) {
         words[K++] = (uint16_t)(x[l] & 0xFFFFu);
         x[l] >>= 16;

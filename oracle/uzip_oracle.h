@@ -89,6 +89,8 @@ void uzo_normalize(const uint32_t cnt[256], uint16_t freq[256]);
  * P:422-424).  words must hold B entries.  Returns the word count K. */
 uint32_t uzo_encode_block(const uint8_t *sym, uint32_t B, const uint16_t freq[256],
                           uint32_t states[32], uint16_t *words);
+uint32_t uzo_encode_block_l(const uint8_t *sym, uint32_t B, const uint16_t freq[256], uint32_t states[32],
+                            uint16_t *words, uint32_t lbits);
 
 /* a8 decode of one block; returns UZO_OK or UZO_ERR_CORRUPT_STREAM. */
 int uzo_decode_block(const uint32_t states_in[32], const uint16_t *words, uint32_t K,

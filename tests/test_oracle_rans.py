@@ -119,3 +119,53 @@ def test_corrupt_block(orc):
     f2 = f.copy(); f2[0x70] += 1; f2[0x7A] -= 1                 # wrong table
     st, out = orc.decode_block(states, words, 4096, f2)
     assert st == orc.ERR_CORRUPT_STREAM or not np.array_equal(out, s)
+
+
+def test_survey_g1_prototype_bytes_at_l16(orc):
+    """The block coder's arithmetic pinned by the survey's independent prototype: with
+    the prototype's state interval [2^16, 2^32) the oracle's coder reproduces its K, block bytes, the first
+    final states and words, and the sha256 of the serialized block.  The format itself uses [2^15, 2^31)
+    (R4: every dividend < 2^31 for exact 32-bit reciprocal division), so only this constant differs from
+    the pinned computation; the L = 2^15 coder is the same function (uzo_encode_block -> _l(15))."""
+    import hashlib
+    s = synth.lcg_symbols(4096, 12345)
+    f = orc.normalize(orc.histogram(s))
+    assert {int(k): int(f[k]) for k in np.nonzero(f > 1)[0]} == {0x72: 2, 0x74: 4, 0x75: 5, 0x76: 5, 0x77: 23,
+                                                                  0x78: 32, 0x79: 59, 0x7a: 118, 0x7b: 234,
+                                                                  0x7c: 491, 0x7d: 936, 0x7e: 1943}
+    states, words = orc.encode_block_l(s, f, 16)
+    assert words.size == 521 and len(orc.block_bytes(states, words)) == 1184
+    assert [int(v) for v in states[:4]] == [0x811780C8, 0x00BC50F2, 0x0023F9CE, 0x2AE5A9DD]
+    # the prototype stores the word groups decoder-forward (round 0 first), UZB1 in emission order
+    # (round R-1 first, R4); regroup by replaying the decoder's word consumption (lanes ascending
+    # within a round either way) -- the sha256 below checks the regrouping as well
+    fwd = _decoder_forward_words(states, words, f, lbits=16)
+    assert [int(v) for v in fwd[:4]] == [0xD2BC, 0xA417, 0xA7A8, 0x337C]
+    assert hashlib.sha256(orc.block_bytes(states, fwd)).hexdigest().startswith("4211ff9cc0691aac9df7c29339159478")
+    # the format's coder is the same function at L = 2^15
+    st15, w15 = orc.encode_block(s, f)
+    st15b, w15b = orc.encode_block_l(s, f, 15)
+    assert np.array_equal(st15, st15b) and np.array_equal(w15, w15b)
+
+
+def _decoder_forward_words(states, words, f, lbits):
+    """Word groups of a coded block reordered round 0 first: replay of the decoder's consumption (O10:
+    per round the k renormalizing lanes take the last k unread words, lanes ascending)."""
+    f = f.astype(np.int64)
+    cdf = np.concatenate([[0], np.cumsum(f)])
+    slot_sym = np.repeat(np.arange(256), f)
+    x = states.astype(np.int64)
+    p = words.size
+    groups = []
+    for _ in range(4096 // 32):
+        slot = x & 4095
+        sy = slot_sym[slot]
+        x = f[sy] * (x >> 12) + slot - cdf[sy]
+        need = x < (1 << lbits)
+        k = int(need.sum())
+        g = words[p - k:p]
+        groups.append(g)
+        x[need] = (x[need] << 16) | g.astype(np.int64)
+        p -= k
+    assert p == 0 and np.all(x == (1 << lbits))
+    return np.concatenate(groups).astype(np.uint16)
