@@ -37,6 +37,9 @@
 #ifndef UZIP_RED_MINB
 #define UZIP_RED_MINB 2   // resident CTAs per SM targeted by reduce launches (r02: 2 without spills beats 3 with)
 #endif
+#ifndef UZIP_ENC_TMA
+#define UZIP_ENC_TMA 0    // A/B: stage each block's input into smem with a TMA bulk copy before the split
+#endif
 #ifndef UZIP_ENC_MINB
 #define UZIP_ENC_MINB 3   // resident CTAs per SM targeted by launches with encode items (measured)
 #endif
@@ -449,7 +452,10 @@ struct FusedCfg {
   static constexpr int kDecTab = 4096 * 4;
   static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce; in P.acc)
   static constexpr int ring(bool) { return 16384; }         // coded tile awaiting its offset
-  static constexpr int smem(bool dec, bool red) { return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0); }
+  static constexpr int kTmaStage = UZIP_ENC_TMA ? B * (int)group_bytes(DT) : 0;  // per warp (A/B only)
+  static constexpr int smem(bool dec, bool red) {
+    return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0) + kWarps * kTmaStage;
+  }
 };
 
 struct FusedShared {
@@ -470,6 +476,8 @@ struct FusedShared {
   // abort words of the other wait sites: each site has its own, so a warp still reading one site's
   // outcome never sees the next site's write (compute-sanitizer racecheck)
   uint32_t ab_credit, ab_table;
+  unsigned long long tma_bar[kWarps];  // A/B (UZIP_ENC_TMA): one mbarrier per warp
+  uint32_t tma_phase[kWarps];
 };
 
 // ---------------------------------------------------------------- E item
@@ -519,7 +527,7 @@ static __device__ void finalize_stream(const EncJob &J, unsigned long long paylo
 // (R-1-j)*32, lanes in order within a row) for the encoder; otherwise element
 // order (the stored-raw payload).  RES: also store the residual plane(s) to
 // every destination (split-send: they leave before the exponents are coded).
-template <int DT, int B, bool RES, bool REV, bool ND1, bool COH = false>
+template <int DT, int B, bool RES, bool REV, bool ND1, bool COH = false, bool SMEM = false>
 __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
                                               uint8_t *buf) {
   using C = FusedCfg<DT, B>;
@@ -536,8 +544,9 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
     uint4 v[C::kBatch];
 #pragma unroll
     for (int i = 0; i < C::kBatch; ++i)
-      v[i] = COH ? ld_cg_v4(src + (size_t)(lane + 32 * (h + i)) * 16)   // written earlier in this launch
-                 : ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
+      v[i] = SMEM  ? *reinterpret_cast<const uint4 *>(src + (size_t)(lane + 32 * (h + i)) * 16)  // TMA-staged
+             : COH ? ld_cg_v4(src + (size_t)(lane + 32 * (h + i)) * 16)   // written earlier in this launch
+                   : ldg_nc_v4(src + (size_t)(lane + 32 * (h + i)) * 16);
 #pragma unroll
     for (int i = 0; i < C::kBatch; ++i) {
       const uint32_t e = (uint32_t)(lane + 32 * (h + i)) * C::kVec;  // element within block
@@ -586,11 +595,30 @@ __device__ __forceinline__ void split_block_t(const EncJob &J, const StreamGeom 
   }
 }
 
-template <int DT, int B, bool RES, bool REV, bool COH = false>
+template <int DT, int B, bool RES, bool REV, bool COH = false, bool SMEM = false>
 __device__ __forceinline__ void split_block(const EncJob &J, const StreamGeom &g, uint64_t b, const uint8_t *src,
                                             uint8_t *buf) {
-  if (!RES || J.nd == 1) split_block_t<DT, B, RES, REV, true, COH>(J, g, b, src, buf);
-  else split_block_t<DT, B, RES, REV, false, COH>(J, g, b, src, buf);
+  if (!RES || J.nd == 1) split_block_t<DT, B, RES, REV, true, COH, SMEM>(J, g, b, src, buf);
+  else split_block_t<DT, B, RES, REV, false, COH, SMEM>(J, g, b, src, buf);
+}
+
+// A/B (UZIP_ENC_TMA): one TMA bulk copy (cp.async.bulk, mbarrier completion) moves the warp's whole
+// input block into its smem stage; the split then reads shared memory instead of issuing LDG.128s.
+__device__ __forceinline__ void tma_stage_block(const uint8_t *src, uint8_t *stage, uint32_t bytes,
+                                                unsigned long long *bar, uint32_t *phase) {
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar), sdst = (uint32_t)__cvta_generic_to_shared(stage);
+  if ((threadIdx.x & 31) == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sdst), "l"(src), "r"(bytes), "r"(sbar) : "memory");
+  }
+  const uint32_t ph = *phase;
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(sbar), "r"(ph) : "memory");
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) *phase = ph ^ 1u;
 }
 
 // a1 for one 16-byte vector of block b that is already in registers (the reduced output of the fused
@@ -1031,7 +1059,14 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   const uint64_t b = b0 + warp;
   if (b < g.n_blocks) {
     // ---- a1: split; the residual goes straight to every destination (split-send)
+#if UZIP_ENC_TMA
+    uint8_t *stage = smem + C::smem(true, false) - (kWarps - warp) * C::kTmaStage;
+    tma_stage_block(J.in + b * (uint64_t)B * group_bytes(DT), stage, (uint32_t)C::kTmaStage, &S.tma_bar[warp],
+                    &S.tma_phase[warp]);
+    split_block<DT, B, true, true, false, true>(J, g, b, stage, buf);
+#else
     split_block<DT, B, true, true>(J, g, b, J.in + b * (uint64_t)B * group_bytes(DT), buf);
+#endif
     __syncwarp();
   }
   code_tile<DT, B, false>(P, J, jidx, t, smem, S, ring, ring_bytes, pd, J.in);
@@ -1516,6 +1551,11 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
   uint8_t *ring = smem + Cf::kEncTab + kWarps * Cf::kWarpBuf;
   EncPending pd{-1, 0};
   const uint64_t nt = P.n_t_items, ne = P.n_e_items, nc = P.n_c_items, total = nt + ne + nc + P.n_d_items;
+  if (UZIP_ENC_TMA && tid < kWarps) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&S.tma_bar[tid])));
+    S.tma_phase[tid] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (tid == 0) {
     S.tile_cnt = 0;
     S.epoch = ld_volatile_u32(P.epoch) & kEpochMask;  // advanced only after every CTA has left
@@ -1635,7 +1675,8 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   const bool dec = p.n_d_items > 0;
   // the ring parks coded tiles (encode launches only; none in the reduce variant)
   p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
-  const int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0);
+  int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0);
+  if (UZIP_ENC_TMA && p.n_e_items > 0) smem = C::smem(true, RED);  // the stages sit at the end of the full layout
   auto kern = k_fused<DT, B, RED, MINB, DONLY>;
   static int attr_set[kMaxDevices] = {0};  // the attribute applies per device
   const int dev = current_device();
