@@ -301,9 +301,9 @@ def run_suites(args, uz, comm, stream, rank, world, local, x, y, role, peer, n):
     weight sync (per tensor and 256 MiB buckets) vs NCCL broadcast, C4 activation allreduce
     256 KiB-256 MiB vs NCCL, C5 allgather / reduce-scatter 1 MiB-4 GiB vs NCCL, KV-cache P2P.
     Every entry: uzip and NCCL algbw (GB/s, nccl-tests convention) and the wire ratio.  Each suite
-    is skipped once the budget (UZIP_BENCH_BUDGET_S, default 900 s) is spent; UZIP_BENCH_SUITES
+    is skipped once the budget (UZIP_BENCH_BUDGET_S, default 300 s) is spent; UZIP_BENCH_SUITES
     selects a comma-separated subset ("none" skips all)."""
-    budget = float(os.environ.get("UZIP_BENCH_BUDGET_S", "900"))
+    budget = float(os.environ.get("UZIP_BENCH_BUDGET_S", "300"))
     want = os.environ.get("UZIP_BENCH_SUITES", "c2_grid,c4_allreduce,c5_ag_rs,kv_p2p,c3_weight_sync")
     t0 = time.time()
     out = {}
@@ -468,10 +468,11 @@ def run_suites(args, uz, comm, stream, rank, world, local, x, y, role, peer, n):
         torch.cuda.empty_cache()
         return res
 
-    suite("c2_grid", c2_grid)
+    # most informative first (the collectives vs NCCL), the 15-communicator C2 grid last
     suite("c4_allreduce", c4_allreduce)
     suite("c5_ag_rs", c5_ag_rs)
     suite("kv_p2p", kv_p2p)
     suite("c3_weight_sync", c3_weight_sync)
+    suite("c2_grid", c2_grid)
     out["budget_s"] = budget
     return out
