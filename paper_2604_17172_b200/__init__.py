@@ -113,6 +113,7 @@ def lib() -> ctypes.CDLL:
                 l.uzip_staged_workspace_bytes.argtypes = [sz, i32, pp]
                 l.uzip_staged_workspace_bytes.restype = sz
                 l.uzip_compress_staged.argtypes = [vp, sz, i32, vp, sz, vp, vp, sz, pp, vp, vp, vp]
+            if hasattr(l, "uzip_nvls_supported"):
                 l.uzip_nvls_supported.argtypes = [i32, ctypes.POINTER(i32)]
                 l.uzip_nvls_selftest.argtypes = [i32, sz]
             if hasattr(l, "uzip_comm_trace"):
