@@ -1043,19 +1043,6 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
   const uint64_t b0 = t * kTileBlocks;
   const uint64_t c = g.n_blocks ? chunk_of(g, b0) : 0;
   const uint64_t key = ((uint64_t)jidx << 48) | c;
-  if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
-    if (!P.tables_ready) {
-      if (tid == 0) {  // the chunk's table: published by its last T item (a smaller ticket)
-        unsigned long long seen = 0;
-        S.ab_table = wait_u64(P, J.tflag + c, kCtlTag | (S.epoch + 1u), seen) ? 0u : 1u;
-      }
-      __syncthreads();
-      if (S.ab_table) return;
-    }
-    tab[tid] = J.enc[c * 256 + tid];  // after the acquire (gpu scope): plain loads see the T item's stores
-    enc_key = key;
-    __syncthreads();
-  }
   const uint64_t b = b0 + warp;
   if (b < g.n_blocks) {
     // ---- a1: split; the residual goes straight to every destination (split-send)
@@ -1068,6 +1055,21 @@ static __device__ void enc_item(const Plan &P, const EncJob &J, int jidx, uint64
     split_block<DT, B, true, true>(J, g, b, J.in + b * (uint64_t)B * group_bytes(DT), buf);
 #endif
     __syncwarp();
+  }
+  // the chunk's table after the split: a table still being built by its T items (small streams) is
+  // waited for while the split's loads and residual stores are already done
+  if (g.n_blocks && key != enc_key) {  // uniform; every warp left the previous tile's table behind
+    if (!P.tables_ready) {
+      if (tid == 0) {  // the chunk's table: published by its last T item (a smaller ticket)
+        unsigned long long seen = 0;
+        S.ab_table = wait_u64(P, J.tflag + c, kCtlTag | (S.epoch + 1u), seen) ? 0u : 1u;
+      }
+      __syncthreads();
+      if (S.ab_table) return;
+    }
+    tab[tid] = J.enc[c * 256 + tid];  // after the acquire (gpu scope): plain loads see the T item's stores
+    enc_key = key;
+    __syncthreads();
   }
   code_tile<DT, B, false>(P, J, jidx, t, smem, S, ring, ring_bytes, pd, J.in);
 }
