@@ -65,7 +65,9 @@ typedef enum {
 
 /* Codec parameters; all-zero (or a NULL pointer) selects the defaults.
  *  block_symbols  B, symbols per independently coded block (Step 2);
- *                 GPU-supported: 1024, 2048, 4096 (default 4096).
+ *                 GPU-supported: 1024, 2048, 4096 (default), 8192, 16384;
+ *                 reduce-scatter / allreduce and uzip_compress_staged take
+ *                 B <= 4096 (UZIP_ERR_INVALID_ARG otherwise).
  *  chunk_blocks   blocks sharing one localized frequency table;
  *                 default 8 MiB of input; must be a multiple of 8.
  *  sample_symbols leading symbols of each chunk that build its table

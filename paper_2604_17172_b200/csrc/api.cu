@@ -26,7 +26,7 @@ uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, 
   if (dtype < 0 || dtype >= kNumDtypes) return UZIP_ERR_UNSUPPORTED_DTYPE;
   const uint32_t eb = group_bytes(dtype);  // input bytes per symbol
   uint32_t B = (p && p->block_symbols) ? p->block_symbols : 4096u;
-  if (!(B == 1024 || B == 2048 || B == 4096)) return UZIP_ERR_INVALID_ARG;
+  if (!gpu_block_ok(B)) return UZIP_ERR_INVALID_ARG;
   const bool global = p && p->global_table;
   uint32_t CB = (p && p->chunk_blocks) ? p->chunk_blocks : (uint32_t)((8u << 20) / (B * eb));
   if (CB == 0 || (!global && CB % kTileBlocks != 0)) return UZIP_ERR_INVALID_ARG;

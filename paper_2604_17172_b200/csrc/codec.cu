@@ -20,24 +20,37 @@ namespace uzip {
 // realistic block is far below it (bf16 weights ~1.4 KB, f16 uniform ~2.8 KB) -- and a larger
 // one (rare) or a raw block is decoded / joined straight from global memory.  With kStage =
 // 3200 and 256-block segments a CTA needs 44 KB, so 5 CTAs (40 warps) fit per SM instead of 4.
+// bf16 blocks (8-bit exponent symbols, ~1.2-1.5 KB coded) stage up to 2176 bytes, so 6 CTAs (48 warps,
+// 40 registers, no spills) fit: 1 GiB bf16 decode 0.578 -> 0.567 ms.  f16 and fp8 symbols carry
+// fraction / second-exponent bits (coded blocks up to ~3.4 KB) and keep 3200 bytes at 5 CTAs; fp32's
+// two residual planes need more registers (at 40 it spills), so it keeps 5 CTAs too.
 #ifndef UZIP_DEC_MINB
 #define UZIP_DEC_MINB 5
 #endif
 #ifndef UZIP_DEC_STAGE
 #define UZIP_DEC_STAGE 3200
 #endif
+#ifndef UZIP_DEC_MINB_EXP8
+#define UZIP_DEC_MINB_EXP8 6
+#endif
+#ifndef UZIP_DEC_STAGE_EXP8
+#define UZIP_DEC_STAGE_EXP8 2176
+#endif
 #ifndef UZIP_DEC_SEG
 #define UZIP_DEC_SEG 256
 #endif
+template <int DT>
 struct DecShared {
+  static constexpr bool kExp8 = DT == kBF16;  // 8-bit exponent symbols, one residual plane
+  static constexpr int kMinB = kExp8 ? UZIP_DEC_MINB_EXP8 : UZIP_DEC_MINB;  // resident CTAs per SM
   static constexpr int kTab = 4096 * 4;              // decode table
   static constexpr int kSeg = UZIP_DEC_SEG;          // blocks per segment (a multiple of 256)
   static constexpr int kOff = kSeg * 4;              // per-segment block offsets (relative to chunk)
-  static constexpr int kStage = UZIP_DEC_STAGE;      // staged payload bytes per warp (multiple of 16)
+  static constexpr int kStage = kExp8 ? UZIP_DEC_STAGE_EXP8 : UZIP_DEC_STAGE;  // staged payload bytes per warp
   static constexpr int kWarpBuf = kStage + 256;      // staged payload + 8-round symbol ring
   static constexpr int kBytes = kTab + kOff + kWarps * kWarpBuf;
+  static_assert(kStage % 16 == 0 && kSeg % 256 == 0, "decoder smem layout");
 };
-static_assert(DecShared::kStage % 16 == 0 && DecShared::kSeg % 256 == 0, "decoder smem layout");
 
 __device__ __forceinline__ void set_err(CodecWs &ws, uint32_t code) { atomicCAS(ws.err, 0u, code); }
 
@@ -53,7 +66,7 @@ __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom 
   bool ok = true;
   if (d == kRawBlock) {
     join_block<DT, B>(src, in, g, b, dst);  // raw symbols joined straight from the stream
-  } else if (size <= (uint32_t)DecShared::kStage) {
+  } else if (size <= (uint32_t)DecShared<DT>::kStage) {
     stage_block(src, size / 16, pay);
     ok = decode_join_warp<DT, B>(pay, d, dtab, ring, in, g, b, dst);
   } else {
@@ -79,20 +92,23 @@ __device__ void decode_block(const uint8_t *__restrict__ in, const StreamGeom &g
   switch (g.B) {
     case 1024: decode_block_t<DT, 1024>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
     case 2048: decode_block_t<DT, 2048>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
+    case 8192: decode_block_t<DT, 8192>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
+    case 16384: decode_block_t<DT, 16384>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
     default: decode_block_t<DT, 4096>(in, g, d, b, off, size, dtab, pay, ring, out, ws); break;
   }
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
+__global__ void __launch_bounds__(256, DecShared<DT>::kMinB) k_decode(const uint8_t *__restrict__ in, uint64_t in_bytes,
                                                   uint8_t *__restrict__ out, uint64_t n, CodecWs ws,
                                                   int32_t *__restrict__ d_status) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t *dtab = reinterpret_cast<uint32_t *>(smem);
-  uint32_t *soff = reinterpret_cast<uint32_t *>(smem + DecShared::kTab);
+  using DS = DecShared<DT>;
+  uint32_t *soff = reinterpret_cast<uint32_t *>(smem + DS::kTab);
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
-  uint8_t *pay = smem + DecShared::kTab + DecShared::kOff + warp * DecShared::kWarpBuf;
-  uint8_t *ring = pay + DecShared::kStage;
+  uint8_t *pay = smem + DS::kTab + DS::kOff + warp * DS::kWarpBuf;
+  uint8_t *ring = pay + DS::kStage;
 
   __shared__ uint32_t s_red[kWarps];
   __shared__ uint32_t s_bad;
@@ -118,7 +134,7 @@ __global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__
     else if (dt != (uint32_t)DT || hn != n) code = UZIP_ERR_SIZE_MISMATCH;
     else if ((flags & ~1u) != 0 || (h[7] & 0xFFFFFF) != (kProbBits | (kLanes << 8) | (kLBits << 16)))
       code = UZIP_ERR_CORRUPT_STREAM;
-    else if (!(B == 1024 || B == 2048 || B == 4096) || CB == 0 || payload > in_bytes)
+    else if (!gpu_block_ok(B) || CB == 0 || payload > in_bytes)
       code = UZIP_ERR_CORRUPT_STREAM;
     else {
       g.init(DT, n, B, CB, S, flags & 1);
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__
       // ---- a7: decode table of chunk c (the shared builder; warp 0's staging buffer is its scratch,
       // free until the bookkeeping barriers below have published the table)
       if (!build_dtab(reinterpret_cast<const uint16_t *>(in + g.off_tab + 512 * c), dtab, s_red,
-                      reinterpret_cast<uint32_t *>(smem + DecShared::kTab + DecShared::kOff))) {
+                      reinterpret_cast<uint32_t *>(smem + DS::kTab + DS::kOff))) {
         set_err(ws, UZIP_ERR_CORRUPT_STREAM);
         break;  // uniform: every warp read the same table
       }
@@ -191,8 +207,8 @@ __global__ void __launch_bounds__(256, UZIP_DEC_MINB) k_decode(const uint8_t *__
       }
       const unsigned long long cbase = coff[c];
       // ---- segments of <= 1024 blocks: exclusive scan of sizes, then decode
-      for (uint64_t seg = s0; seg < chunk_stop; seg += DecShared::kSeg) {
-        const uint64_t seg_end = min(chunk_stop, seg + (uint64_t)DecShared::kSeg);
+      for (uint64_t seg = s0; seg < chunk_stop; seg += DS::kSeg) {
+        const uint64_t seg_end = min(chunk_stop, seg + (uint64_t)DS::kSeg);
         const unsigned long long run0 = s_base;
         unsigned long long run = run0;
         for (uint64_t bb0 = seg; bb0 < seg_end; bb0 += 256) {
@@ -287,15 +303,15 @@ cudaError_t launch_decode_t(const void *in, uint64_t in_bytes, void *out, uint64
   static bool attr[kMaxDev] = {false};  // per device
   const int dev = cur_dev();
   if (!attr[dev]) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecShared::kBytes);
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecShared<DT>::kBytes);
     if (e != cudaSuccess) return e;
     attr[dev] = true;
   }
-  int grid = sm_count() * occupancy(kern, 256, DecShared::kBytes);
+  int grid = sm_count() * occupancy(kern, 256, DecShared<DT>::kBytes);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   const uint64_t want = (est_blocks + kWarps - 1) / kWarps;  // >= one block per warp: one table build per 8 blocks
   if ((uint64_t)grid > want) grid = (int)(want ? want : 1);
-  kern<<<grid, 256, DecShared::kBytes, st>>>((const uint8_t *)in, in_bytes, (uint8_t *)out, n, ws, d_status);
+  kern<<<grid, 256, DecShared<DT>::kBytes, st>>>((const uint8_t *)in, in_bytes, (uint8_t *)out, n, ws, d_status);
   return cudaGetLastError();
 }
 }  // namespace

@@ -429,9 +429,11 @@ uzip_status_t ensure_acc(uzip_comm *c) {
 uzip_status_t check_dtype(uzip_dtype_t dt) {
   return ((int)dt < 0 || (int)dt >= kNumDtypes) ? UZIP_ERR_UNSUPPORTED_DTYPE : UZIP_OK;
 }
-// reductions are defined for bf16/f16/f32 only (R22)
-uzip_status_t check_reduce_dtype(uzip_dtype_t dt) {
-  return ((int)dt < 0 || (int)dt > kF32) ? UZIP_ERR_UNSUPPORTED_DTYPE : UZIP_OK;
+// reductions are defined for bf16/f16/f32 only (R22); the reduce kernel's fp32 accumulators hold
+// blocks of at most kMaxB symbols (larger blocks: codec, P2P, allgather, all-to-all, broadcast only)
+uzip_status_t check_reduce_dtype(uzip_comm_t c, uzip_dtype_t dt) {
+  if ((int)dt < 0 || (int)dt > kF32) return UZIP_ERR_UNSUPPORTED_DTYPE;
+  return c->cfg.codec.block_symbols > kMaxB ? UZIP_ERR_INVALID_ARG : UZIP_OK;
 }
 
 }  // namespace
@@ -637,7 +639,7 @@ uzip_status_t uzip_reduce_scatter(const void *sendbuf, void *recvbuf, size_t rec
                                   uzip_op_t op, uzip_comm_t c, void *stream) {
   NvtxRange nvtx_range("uzip_reduce_scatter");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
-  if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
+  if (uzip_status_t s = check_reduce_dtype(c, dtype)) return s;
   if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
   if (recvcount == 0) return UZIP_OK;
   if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return UZIP_ERR_INVALID_ARG;
@@ -684,7 +686,7 @@ uzip_status_t uzip_allreduce(const void *sendbuf, void *recvbuf, size_t count, u
                              uzip_comm_t c, void *stream) {
   NvtxRange nvtx_range("uzip_allreduce");
   if (!valid(c)) return UZIP_ERR_INVALID_ARG;
-  if (uzip_status_t s = check_reduce_dtype(dtype)) return s;
+  if (uzip_status_t s = check_reduce_dtype(c, dtype)) return s;
   if ((int)op < 0 || (int)op > UZIP_MAX) return UZIP_ERR_INVALID_ARG;
   if (count == 0) return UZIP_OK;
   const int N = c->nranks, me = c->rank, dt = (int)dtype;

@@ -1744,6 +1744,12 @@ cudaError_t preload_t() {
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 1024, false, UZIP_DEC_ONLY_MINB, true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 2048, false, UZIP_DEC_ONLY_MINB, true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 4096, false, UZIP_DEC_ONLY_MINB, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 8192, false, UZIP_ENC_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 8192, false, UZIP_DEC_ONLY_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 8192, false, UZIP_DEC_ONLY_MINB, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 16384, false, UZIP_ENC_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 16384, false, UZIP_DEC_ONLY_MINB>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_fused<DT, 16384, false, UZIP_DEC_ONLY_MINB, true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_hist<DT>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_norm<DT>);
   }
@@ -1755,7 +1761,17 @@ cudaError_t launch_fused_b(const Plan &p, uint32_t B, cudaStream_t st, int max_c
   switch (B) {
     case 1024: return launch_fused_t<DT, 1024, RED>(p, st, max_ctas);
     case 2048: return launch_fused_t<DT, 2048, RED>(p, st, max_ctas);
-    default: return launch_fused_t<DT, 4096, RED>(p, st, max_ctas);
+    case 4096: return launch_fused_t<DT, 4096, RED>(p, st, max_ctas);
+    default:
+      // larger blocks (C2 block sweep): codec, P2P, allgather, all-to-all, broadcast; the reduce
+      // kernel's accumulators hold kMaxB symbols per warp (the C ABI rejects larger B for reductions)
+      if constexpr (RED) {
+        return cudaErrorInvalidValue;
+      } else {
+        if (B == 8192) return launch_fused_t<DT, 8192, RED>(p, st, max_ctas);
+        if (B == 16384) return launch_fused_t<DT, 16384, RED>(p, st, max_ctas);
+        return cudaErrorInvalidValue;
+      }
   }
 }
 

@@ -233,6 +233,7 @@ uzip_status_t staged_geom(size_t count, uzip_dtype_t dtype, const uzip_codec_par
   if (!(dtype == UZIP_BF16 || dtype == UZIP_F16 || dtype == UZIP_F32)) return UZIP_ERR_UNSUPPORTED_DTYPE;
   uzip_codec_params_t p = params ? *params : uzip_codec_params_t{0, 0, 0, 0};
   p.global_table = 1;  // Step 1 builds one global table
+  if (p.block_symbols > kMaxB) return UZIP_ERR_INVALID_ARG;  // the ablation pipeline: B <= 4096
   return resolve_geom((int)dtype, count, &p, g);
 }
 

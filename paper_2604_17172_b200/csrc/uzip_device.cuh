@@ -22,7 +22,12 @@ constexpr uint32_t kRawBlock = 0xFFFFFFFFu;
 constexpr uint32_t kVersion = 1;
 constexpr int kWarps = 8;                       // warps per CTA in the codec kernels
 constexpr uint32_t kTileBlocks = kWarps;        // blocks per look-back tile
-constexpr uint32_t kMaxB = 4096;                // largest block the GPU kernels stage in smem
+constexpr uint32_t kMaxB = 4096;                // largest block of the reduce kernels (fp32 accumulators)
+constexpr uint32_t kMaxCodecB = 16384;          // largest block of the codec / P2P / allgather kernels
+// block sizes the GPU kernels are instantiated for (C2 block sweep)
+__host__ __device__ constexpr bool gpu_block_ok(uint32_t B) {
+  return B == 1024 || B == 2048 || B == 4096 || B == 8192 || B == 16384;
+}
 
 enum Dtype : int { kBF16 = 0, kF16 = 1, kF32 = 2, kE4M3 = 3, kE5M2 = 4 };
 constexpr int kNumDtypes = 5;

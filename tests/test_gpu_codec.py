@@ -353,3 +353,29 @@ def test_nvls_multicast_primitive(uz):
     if st == uz.ERR_NOT_IMPLEMENTED:
         pytest.skip("cuMulticastCreate refused on this node (single visible GPU / no multicast team)")
     assert st == 0
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32, E4M3, E5M2])
+@pytest.mark.parametrize("B", [8192, 16384])
+def test_large_blocks_equal_oracle(uz, orc, dtype, B):
+    """Blocks of 8192 / 16384 symbols (the C2 block sweep): several tiles, several table
+    chunks (chunk_blocks=8), a stored-raw block and a ragged tail; stream bytes == oracle's, exact
+    round trip.  Coded blocks this large exceed the decoder's smem staging, so they are decoded in
+    place from global memory (the rare path of the 4096-symbol format)."""
+    per = 2 if dtype == E4M3 else 1  # elements per symbol
+    n = per * (20 * B + 11)
+    bits = synth.normal(n, 0.02, 31 + B, dtype)
+    bits[per * B * 9:per * B * 10] = synth.random_bits(per * B, 5, dtype)
+    for params in (dict(block_symbols=B), dict(block_symbols=B, chunk_blocks=8)):
+        ref = orc.compress(dtype, bits, **params)
+        got = gpu_compress(uz, bits, dtype, **params)
+        assert got == ref, params
+        st, back = gpu_decompress(uz, got, n, dtype)
+        assert st == 0 and np.array_equal(back, bits)
+
+
+def test_unsupported_block_sizes_rejected(uz):
+    x = torch.zeros(1 << 16, dtype=torch.bfloat16, device="cuda")
+    for B in (512, 3072, 32768):
+        with pytest.raises(uz.UzipError):
+            uz.compress(x, block_symbols=B)

@@ -823,3 +823,31 @@ def test_collective_wire_streams_equal_oracle(uz, orc, kind, nr):
             assert g.comms[d].read_staging(s, 0, len(blob)) == blob, (s, d)
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("B", [8192, 16384])
+def test_large_blocks_p2p_allgather(uz, orc, B):
+    """Blocks of 8192 / 16384 symbols through the communicator (C2 block sweep): the P2P wire stream
+    == the oracle's with the same params, allgather bit-exact; reductions reject B > 4096."""
+    nr = 2
+    g = Group(uz, nr, staging_bytes=64 << 20, min_compress_bytes=1, block_symbols=B)
+    try:
+        n = 3 * (1 << 20) + B * 7 + 11
+        bits = synth.weights(n, 77 + B)
+        x = dev(bits, BF16)
+        y = torch.empty_like(x)
+        g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else c.recv(y, 0, s))
+        assert np.array_equal(host(y, BF16), bits)
+        ref = orc.compress(BF16, bits, block_symbols=B)
+        assert g.comms[1].read_staging(0, 0, len(ref)) == ref
+        m = (1 << 20) + 3 * B + 5
+        ins = [synth.weights(m, 500 + r) for r in range(nr)]
+        xs = [dev(b, BF16) for b in ins]
+        outs = [torch.empty(nr * m, dtype=torch.bfloat16, device="cuda") for _ in range(nr)]
+        g.run(lambda r, c, s: c.all_gather(outs[r], xs[r], s))
+        for r in range(nr):
+            assert np.array_equal(host(outs[r], BF16), np.concatenate(ins))
+        with pytest.raises(uz.UzipError):
+            g.comms[0].all_reduce(outs[0], outs[0])
+    finally:
+        g.close()

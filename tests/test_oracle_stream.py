@@ -50,8 +50,23 @@ def test_roundtrip_multichunk_and_global(orc, dtype):
     s_global = _roundtrip(orc, dtype, bits, global_table=True)
     hd = orc.parse_header(s_global)
     assert hd["flags"] == 1 and hd["n_chunks"] == 1 and hd["CB"] == 37
-    for B in (32, 1024, 2048, 8192):
+    for B in (32, 1024, 2048, 8192, 16384):
         _roundtrip(orc, dtype, bits, block_symbols=B)
+
+
+def test_ratio_large_blocks(orc):
+    """C2 block sweep: a block carries 128 bytes of final lane states, so the ratio of
+    W bf16 falls with B (4096 > 8192 > 16384) by about those state bytes, and stays above the
+    closed-form Shannon bound."""
+    n = 1 << 22
+    bits = synth.normal(n, 0.02, 5, BF16)
+    r = {B: len(_roundtrip(orc, BF16, bits, block_symbols=B)) / (2 * n) for B in (4096, 8192, 16384)}
+    assert r[4096] > r[8192] > r[16384]
+    for B in (8192, 16384):
+        saved = (n // 4096 - n // B) * 128 / (2 * n)  # fewer blocks, fewer state headers
+        assert abs((r[4096] - r[B]) - saved) < 0.002, (B, r)
+    H = _entropy(_normal_symbol_probs(0.02))
+    assert r[16384] >= (RES_BITS[BF16] + H) / (8 * EB[BF16]) - 0.002
 
 
 def test_adversarial_chunk_floor(orc):
