@@ -299,6 +299,87 @@ __device__ __forceinline__ bool decode_join_warp_epi(const uint8_t *pay, uint32_
   return !(p != 0 || __any_sync(0xFFFFFFFFu, x != kL));
 }
 
+// Two coded blocks per warp, their rANS chains interleaved round by round (a8): the decoder is bound by
+// the latency of its table-lookup -> renormalization -> word-fetch chain, and a second independent
+// chain in the same warp hides half of it.  One residual plane of one byte per symbol (bf16, f16,
+// e4m3): pays / rings / residual prefetches per block; `ok` reports each block.
+template <int DT, int B>
+__device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t KA, const uint8_t *payB, uint32_t KB,
+                                                  const uint32_t *dtab, uint8_t *ringA, uint8_t *ringB,
+                                                  const uint8_t *stream, const StreamGeom &g, uint64_t bA,
+                                                  uint64_t bB, uint8_t *dstA, uint8_t *dstB, bool &okA, bool &okB) {
+  static_assert(DT == kBF16 || DT == kF16 || DT == kE4M3, "one residual byte per symbol");
+  constexpr int kGroups = B / 256;
+  constexpr int kPF = 2;  // residual prefetch distance in groups, per block
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint16_t *wA = reinterpret_cast<const uint16_t *>(payA) + 64;
+  const uint16_t *wB = reinterpret_cast<const uint16_t *>(payB) + 64;
+  const uint8_t *resA = stream + g.off_res0 + bA * B + 8 * lane;
+  const uint8_t *resB = stream + g.off_res0 + bB * B + 8 * lane;
+  uint2 rA[kPF], rB[kPF];
+#pragma unroll
+  for (int i = 0; i < kPF; ++i) {
+    rA[i] = ld_cg_v2(resA + 256 * i);
+    rB[i] = ld_cg_v2(resB + 256 * i);
+  }
+  uint32_t xA = reinterpret_cast<const uint32_t *>(payA)[lane], xB = reinterpret_cast<const uint32_t *>(payB)[lane];
+  int32_t pA = (int32_t)KA, pB = (int32_t)KB;
+#pragma unroll 1
+  for (int g0 = 0; g0 < kGroups; g0 += kPF) {
+#pragma unroll
+    for (int q = 0; q < kPF; ++q) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t eA = dtab[xA & (kM - 1)];
+        const uint32_t eB = dtab[xB & (kM - 1)];
+        ringA[u * 32 + lane] = (uint8_t)eA;
+        ringB[u * 32 + lane] = (uint8_t)eB;
+        xA = (eA >> 20) * (xA >> kProbBits) + ((eA >> 8) & 0xFFFu);
+        xB = (eB >> 20) * (xB >> kProbBits) + ((eB >> 8) & 0xFFFu);
+        const bool nA = xA < kL, nB = xB < kL;
+        const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nA), mB = __ballot_sync(0xFFFFFFFFu, nB);
+        pA -= __popc(mA);
+        pB -= __popc(mB);
+        const uint32_t wa = wA[max(pA + __popc(mA & lt), 0)], wb = wB[max(pB + __popc(mB & lt), 0)];
+        xA = nA ? ((xA << 16) | wa) : xA;
+        xB = nB ? ((xB << 16) | wb) : xB;
+      }
+      __syncwarp();
+      const int gi = g0 + q;
+      const uint32_t e0 = 256 * gi + 8 * lane;
+      const uint2 sA = *reinterpret_cast<const uint2 *>(ringA + 8 * lane);
+      const uint2 sB = *reinterpret_cast<const uint2 *>(ringB + 8 * lane);
+      uint4 vA, vB;
+      if (DT == kBF16) {
+        join4_bf16(sA.x, rA[q].x, vA.x, vA.y);
+        join4_bf16(sA.y, rA[q].y, vA.z, vA.w);
+        join4_bf16(sB.x, rB[q].x, vB.x, vB.y);
+        join4_bf16(sB.y, rB[q].y, vB.z, vB.w);
+      } else if (DT == kE4M3) {
+        join4_e4m3(sA.x, rA[q].x, vA.x, vA.y);
+        join4_e4m3(sA.y, rA[q].y, vA.z, vA.w);
+        join4_e4m3(sB.x, rB[q].x, vB.x, vB.y);
+        join4_e4m3(sB.y, rB[q].y, vB.z, vB.w);
+      } else {
+        join4_f16(sA.x, rA[q].x, vA.x, vA.y);
+        join4_f16(sA.y, rA[q].y, vA.z, vA.w);
+        join4_f16(sB.x, rB[q].x, vB.x, vB.y);
+        join4_f16(sB.y, rB[q].y, vB.z, vB.w);
+      }
+      st_any16(dstA + 2 * e0, vA);
+      st_any16(dstB + 2 * e0, vB);
+      if (gi + kPF < kGroups) {
+        rA[q] = ld_cg_v2(resA + 256 * (gi + kPF));
+        rB[q] = ld_cg_v2(resB + 256 * (gi + kPF));
+      }
+      __syncwarp();
+    }
+  }
+  okA = !(pA != 0 || __any_sync(0xFFFFFFFFu, xA != kL));
+  okB = !(pB != 0 || __any_sync(0xFFFFFFFFu, xB != kL));
+}
+
 template <int DT, int B>
 __device__ __forceinline__ bool decode_join_warp(const uint8_t *pay, uint32_t K, const uint32_t *dtab,
                                                  uint8_t *ring, const uint8_t *stream, const StreamGeom &g,
