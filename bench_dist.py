@@ -284,6 +284,33 @@ def versions():
     return v
 
 
+def nvlink_bytes(index):
+    """(tx, rx) NVLink data bytes of GPU `index` so far, summed over its links (NVML throughput
+    counters, KiB), or None where NVML or the counters are unavailable (no NVLink, one-GPU boxes)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        tx = rx = 0
+        seen = False
+        for link in range(18):
+            try:
+                if pynvml.nvmlDeviceGetNvLinkState(h, link) != pynvml.NVML_FEATURE_ENABLED:
+                    continue
+            except pynvml.NVMLError:
+                continue
+            vals = pynvml.nvmlDeviceGetFieldValues(h, [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                                                       (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+            if vals[0].nvmlReturn or vals[1].nvmlReturn:
+                continue
+            tx += vals[0].value.ullVal * 1024
+            rx += vals[1].value.ullVal * 1024
+            seen = True
+        return (tx, rx) if seen else None
+    except Exception:
+        return None
+
+
 def _fill_w(buf, seed):
     """W = bf16(N(0, 0.02)) in 64 Mi-element slices (no fp32 temporary of the whole buffer)."""
     g = torch.Generator(device="cuda")
@@ -339,10 +366,16 @@ def run_suites(args, uz, comm, stream, rank, world, local, x, y, role, peer, n):
             out[name] = {"skipped": f"time budget {budget:.0f} s spent"}
             return
         ts = time.time()
+        nv0 = nvlink_bytes(local)
         out[name] = fn()
         torch.cuda.synchronize()
         dist.barrier()
         out[name]["seconds"] = round(time.time() - ts, 1)
+        nv1 = nvlink_bytes(local)
+        # this rank's NVLink data bytes over the whole suite (uzip and NCCL legs): counter evidence that
+        # the traffic went over NVLink, not a per-leg number
+        out[name]["nvlink_GB_rank"] = (None if nv0 is None or nv1 is None else
+                                       {"tx": round((nv1[0] - nv0[0]) / 1e9, 3), "rx": round((nv1[1] - nv0[1]) / 1e9, 3)})
 
     pairs = world // 2
 

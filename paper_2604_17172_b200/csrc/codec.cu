@@ -44,6 +44,9 @@ namespace uzip {
 #ifndef UZIP_DEC_PAIR
 #define UZIP_DEC_PAIR 1
 #endif
+#ifndef UZIP_DEC_MINB_F32
+#define UZIP_DEC_MINB_F32 4  // fp32 (two residual planes): 64 registers without spills (5 CTAs spilled)
+#endif
 #ifndef UZIP_DEC_PAIR_MINB
 #define UZIP_DEC_PAIR_MINB 5  // register budget (48); smem holds 4 CTAs
 #endif
@@ -57,7 +60,8 @@ template <int DT>
 struct DecShared {
   static constexpr bool kExp8 = DT == kBF16;  // 8-bit exponent symbols, one residual plane
   static constexpr bool kPair = kExp8 && UZIP_DEC_PAIR;  // two blocks per warp (two staging areas)
-  static constexpr int kMinB = kPair ? UZIP_DEC_PAIR_MINB : kExp8 ? UZIP_DEC_MINB_EXP8 : UZIP_DEC_MINB;
+  static constexpr int kMinB = kPair ? UZIP_DEC_PAIR_MINB : kExp8 ? UZIP_DEC_MINB_EXP8
+                              : DT == kF32 ? UZIP_DEC_MINB_F32 : UZIP_DEC_MINB;
   static constexpr int kTab = 4096 * 4;              // decode table
   static constexpr int kSeg = UZIP_DEC_SEG;          // blocks per segment (a multiple of 256)
   static constexpr int kOff = kSeg * 4;              // per-segment block offsets (relative to chunk)
@@ -84,7 +88,7 @@ __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom 
     join_block<DT, B>(src, in, g, b, dst);  // raw symbols joined straight from the stream
   } else if (size <= (uint32_t)DecShared<DT>::kStage) {
     stage_block(src, size / 16, pay);
-    ok = decode_join_warp<DT, B>(pay, d, dtab, ring, in, g, b, dst);
+    ok = decode_join_warp<DT, B, UZIP_DEC_NOCLAMP != 0 && DT != kF32>(pay, d, dtab, ring, in, g, b, dst);
   } else {
     // rare: a coded block larger than the staging area is decoded in place from global memory
     // (word indices never leave [0, K), so even a corrupt stream is read in bounds)
