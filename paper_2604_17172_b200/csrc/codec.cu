@@ -20,7 +20,8 @@ namespace uzip {
 // realistic block is far below it (bf16 weights ~1.4 KB, f16 uniform ~2.8 KB) -- and a larger
 // one (rare) or a raw block is decoded / joined straight from global memory.  With kStage =
 // 3200 and 256-block segments a CTA needs 44 KB, so 5 CTAs (40 warps) fit per SM instead of 4.
-// bf16 blocks (8-bit exponent symbols, ~1.2-1.5 KB coded) stage up to 2176 bytes, so 6 CTAs (48 warps,
+// (Round 2: 3584 bytes for f16 / fp8 / fp32 at 4 CTAs -- 256 MiB U[-1,1] f16 decode 0.161 -> 0.151 ms,
+// e4m3 0.179 -> 0.164 ms.)  bf16 blocks (8-bit exponent symbols, ~1.2-1.5 KB coded) stage up to 2176 bytes, so 6 CTAs (48 warps,
 // 40 registers, no spills) fit: 1 GiB bf16 decode 0.578 -> 0.567 ms.  f16 and fp8 symbols carry
 // fraction / second-exponent bits (coded blocks up to ~3.4 KB) and keep 3200 bytes at 5 CTAs; fp32's
 // two residual planes need more registers (at 40 it spills), so it keeps 5 CTAs too.
@@ -28,7 +29,7 @@ namespace uzip {
 #define UZIP_DEC_MINB 5
 #endif
 #ifndef UZIP_DEC_STAGE
-#define UZIP_DEC_STAGE 3200
+#define UZIP_DEC_STAGE 3584  // f16 / fp8 / fp32 (4 CTAs): U[-1,1] f16 blocks (~2.7 KB, some larger) stay staged
 #endif
 #ifndef UZIP_DEC_MINB_EXP8
 #define UZIP_DEC_MINB_EXP8 6

@@ -40,6 +40,9 @@
 #ifndef UZIP_ENC_TMA
 #define UZIP_ENC_TMA 0    // A/B: stage each block's input into smem with a TMA bulk copy before the split
 #endif
+#ifndef UZIP_RING_WIDE
+#define UZIP_RING_WIDE 24576  // ring bytes of f16 / fp8 encode launches (bf16 / fp32 and reduce: 16 KiB)
+#endif
 #ifndef UZIP_ENC_MINB
 #define UZIP_ENC_MINB 3   // resident CTAs per SM targeted by launches with encode items (measured)
 #endif
@@ -451,7 +454,12 @@ struct FusedCfg {
   static constexpr int kWarpBuf = B + 256;                  // per warp: symbols/words (E) or payload + ring (D)
   static constexpr int kDecTab = 4096 * 4;
   static constexpr int kAcc = 4 * B;                        // fp32 accumulator per warp (reduce; in P.acc)
-  static constexpr int ring(bool) { return 16384; }         // coded tile awaiting its offset
+  // coded tile awaiting its offset: 16 KiB hold a bf16 / fp32 tile (8-bit exponents, ~1.5 KB per coded
+  // block); f16 and fp8 symbols carry more bits (~2.3-2.8 KB per block on U[-1,1]), so their encode
+  // launches park up to 24 KiB -- a tile larger than the ring finishes its look-back before it is stored
+  static constexpr int ring(bool red) {
+    return (!red && (DT == kF16 || DT == kE4M3 || DT == kE5M2)) ? UZIP_RING_WIDE : 16384;
+  }
   static constexpr int kTmaStage = UZIP_ENC_TMA ? B * (int)group_bytes(DT) : 0;  // per warp (A/B only)
   static constexpr int smem(bool dec, bool red) {
     return kEncTab + kWarps * kWarpBuf + ring(red) + (dec ? kDecTab : 0) + kWarps * kTmaStage;
@@ -1676,7 +1684,8 @@ cudaError_t launch_fused_k(Plan p, cudaStream_t st, int max_ctas) {
   using C = FusedCfg<DT, B>;
   const bool dec = p.n_d_items > 0;
   // the ring parks coded tiles (encode launches only; none in the reduce variant)
-  p.ring_bytes = (p.n_e_items > 0) ? C::ring(RED) : 0;
+  // (launches that also decode keep 16 KiB: their decode table follows the ring, 3 CTAs per SM)
+  p.ring_bytes = (p.n_e_items > 0) ? (dec ? 16384 : C::ring(RED)) : 0;
   int smem = C::kEncTab + kWarps * C::kWarpBuf + p.ring_bytes + ((dec || RED) ? C::kDecTab : 0);
   if (UZIP_ENC_TMA && p.n_e_items > 0) smem = C::smem(true, RED);  // the stages sit at the end of the full layout
   auto kern = k_fused<DT, B, RED, MINB, DONLY>;
