@@ -309,7 +309,7 @@ __device__ __forceinline__ bool decode_join_warp_epi(const uint8_t *pay, uint32_
 // the latency of its table-lookup -> renormalization -> word-fetch chain, and a second independent
 // chain in the same warp hides half of it.  One residual plane of one byte per symbol (bf16, f16,
 // e4m3): pays / rings / residual prefetches per block; `ok` reports each block.
-template <int DT, int B>
+template <int DT, int B, bool NOCLAMP = (UZIP_DEC_NOCLAMP != 0)>
 __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t KA, const uint8_t *payB, uint32_t KB,
                                                   const uint32_t *dtab, uint8_t *ringA, uint8_t *ringB,
                                                   const uint8_t *stream, const StreamGeom &g, uint64_t bA,
@@ -347,14 +347,11 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
         const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nA), mB = __ballot_sync(0xFFFFFFFFu, nB);
         pA -= __popc(mA);
         pB -= __popc(mB);
-#if UZIP_DEC_NOCLAMP
-        // staged in k_decode's shared memory: a corrupt stream drives p below 0 by at most B words, which
-        // stays inside the CTA's window (the payload areas sit above the 17 KB table + offsets); p != 0 at
-        // the end reports it
-        const uint32_t wa = wA[pA + __popc(mA & lt)], wb = wB[pB + __popc(mB & lt)];
-#else
-        const uint32_t wa = wA[max(pA + __popc(mA & lt), 0)], wb = wB[max(pB + __popc(mB & lt), 0)];
-#endif
+        // NOCLAMP (k_decode): a corrupt stream drives p below 0 by at most B words, which stays inside
+        // the CTA's shared memory (the payload areas sit above the 17 KB table + offsets); p != 0 at the
+        // end reports it.  k_fused's layout clamps.
+        const int32_t ia = pA + __popc(mA & lt), ib = pB + __popc(mB & lt);
+        const uint32_t wa = wA[NOCLAMP ? ia : max(ia, 0)], wb = wB[NOCLAMP ? ib : max(ib, 0)];
         xA = nA ? ((xA << 16) | wa) : xA;
         xB = nB ? ((xB << 16) | wb) : xB;
       }

@@ -1301,6 +1301,110 @@ static __device__ void dec_item(const Plan &P, const DecJob &J, int jidx, uint64
   dec_done(P, J, jidx, t);
 }
 
+// Two consecutive tiles of a plain decode job at once (the D-item form of k_decode's pairing): every
+// warp decodes block w of tile t and block w of tile t + 1 with their rANS chains interleaved
+// (decode_join_warp2), both staged in the warp's buffer (two halves); blocks that are raw or larger
+// than a half take the one-chain path.  The caller checked pair_tiles().
+#ifndef UZIP_DEC_PAIR_TILES
+#define UZIP_DEC_PAIR_TILES 1
+#endif
+template <int DT, int B, bool RED>
+constexpr bool kDecPairOk = UZIP_DEC_PAIR_TILES && !RED && B == 4096 && (DT == kBF16 || DT == kF16 || DT == kE4M3);
+
+__device__ __forceinline__ bool pair_tiles(const DecJob &J, uint64_t t) {
+  const StreamGeom &g = J.g;
+  return !J.raw && J.nfwd == 0 && J.nsrc == 1 && (t + 1) * kTileBlocks < g.n_blocks &&
+         chunk_of(g, t * kTileBlocks) == chunk_of(g, (t + 1) * kTileBlocks);
+}
+
+template <int DT, int B>
+static __device__ void dec_item2(const Plan &P, const DecJob &J, int jidx, uint64_t t, uint8_t *smem,
+                                 FusedShared &S, uint64_t &dec_key) {
+  using C = FusedCfg<DT, B>;
+  constexpr uint32_t kHalf = C::kWarpBuf / 2, kStage2 = (kHalf - 256) & ~15u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
+  const StreamGeom &g = J.g;
+  const uint64_t b0 = t * kTileBlocks;
+  const uint64_t c = chunk_of(g, b0);
+  const uint64_t key = (1ull << 63) | ((uint64_t)jidx << 48) | c;
+  const bool need_table = key != dec_key;
+  if (tid == 0) {
+    acquire_tile(P, J, 0, t, need_table, S);
+    trace_ev(P, kTrDAcq, (uint32_t)jidx, t);
+    if (!S.abort) {
+      const unsigned long long o0 = S.src_off[0];
+      acquire_tile(P, J, 0, t + 1, false, S);
+      trace_ev(P, kTrDAcq, (uint32_t)jidx, t + 1);
+      S.red64[0] = S.src_off[0];  // (scratch word: a new FusedShared field measurably raised k_fused's spills)
+      S.src_off[0] = o0;
+    }
+  }
+  __syncthreads();
+  if (S.abort) return;
+  const uint8_t *stream = J.src[0];
+  uint32_t *dtab = reinterpret_cast<uint32_t *>(smem + C::kEncTab + kWarps * C::kWarpBuf + P.ring_bytes);
+  if (need_table) {
+    if (!build_dtab(reinterpret_cast<const uint16_t *>(stream + g.off_tab + 512 * c), dtab, S.red,
+                    reinterpret_cast<uint32_t *>(smem + C::kEncTab))) {
+      if (tid == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+      dec_key = ~0ull;
+      return;
+    }
+    dec_key = key;
+  }
+  __syncthreads();
+  uint8_t *buf = smem + C::kEncTab + warp * C::kWarpBuf;
+  uint32_t KA, KB;
+  unsigned long long offA, offB, endA, endB;
+  bool badA, badB;
+  tile_block(stream, g, b0, warp, S.src_off[0], KA, offA, endA, badA);
+  tile_block(stream, g, b0 + kTileBlocks, warp, S.red64[0], KB, offB, endB, badB);
+  (void)endA;
+  const uint64_t bA = b0 + warp, bB = b0 + kTileBlocks + warp;
+  const bool okA = bA < g.n_blocks && !badA, okB = bB < g.n_blocks && !badB;
+  const uint32_t sA = KA == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * KA);
+  const uint32_t sB = KB == kRawBlock ? (uint32_t)B : (uint32_t)round16(128 + 2ull * KB);
+  bool bad = badA || badB;
+  if (okA && okB && KA != kRawBlock && KB != kRawBlock && sA <= kStage2 && sB <= kStage2) {
+    uint8_t *payB = buf + kHalf;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(buf), s1 = (uint32_t)__cvta_generic_to_shared(payB);
+    const uint8_t *srcA = stream + g.off_pay + offA, *srcB = stream + g.off_pay + offB;
+    for (uint32_t i = lane; i < sA / 16; i += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + 16 * i), "l"(srcA + 16 * i) : "memory");
+    for (uint32_t i = lane; i < sB / 16; i += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s1 + 16 * i), "l"(srcB + 16 * i) : "memory");
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    bool gA, gB;
+    decode_join_warp2<DT, B, false>(buf, KA, payB, KB, dtab, buf + kStage2, payB + kStage2, stream, g, bA, bB,
+                                    J.out + bA * (uint64_t)B * g.eb, J.out + bB * (uint64_t)B * g.eb, gA, gB);
+    bad = bad || !gA || !gB;
+    __syncwarp();
+  } else {
+    for (int h = 0; h < 2; ++h) {
+      const bool ok = h ? okB : okA;
+      if (!ok) continue;
+      const uint32_t K = h ? KB : KA, size = h ? sB : sA;
+      const uint64_t b = h ? bB : bA;
+      stage_payload(stream, g, h ? offB : offA, size, buf);
+      uint8_t *dst = J.out + b * (uint64_t)B * g.eb;
+      if (K == kRawBlock) join_block<DT, B>(buf, stream, g, b, dst);
+      else if (!decode_join_warp<DT, B>(buf, K, dtab, buf + B, stream, g, b, dst)) bad = true;
+      __syncwarp();
+    }
+  }
+  if (bad && lane == 0) raise_err(P, UZIP_ERR_CORRUPT_STREAM);
+  if (t + 1 == J.ntiles - 1) {  // raw tail
+    const uint64_t tail_bytes = g.tail_bytes();
+    const uint8_t *tsrc = stream + g.off_tail(endB);
+    uint8_t *tdst = J.out + g.n_coded * g.eb;
+    for (uint64_t i = tid; i < tail_bytes; i += 256) tdst[i] = tsrc[i];
+  }
+  __syncthreads();
+  dec_done(P, J, jidx, t);
+  dec_done(P, J, jidx, t + 1);
+}
+
 // The warp's fp32 accumulator lives in global memory (P.acc, B floats per
 // (CTA, warp), L2-resident): every lane reads and writes only its own 8-element
 // groups, the same ones for every source, so it is thread-private data moved
@@ -1585,6 +1689,13 @@ __global__ void __launch_bounds__(256, MINB) k_fused(const __grid_constant__ Pla
       const DecJob &Jd = P.d[j];
       const uint64_t r = Jd.run > 1 ? Jd.run : 1, t1 = min(Jd.ntiles, (k + 1) * r);
       for (uint64_t t = k * r; t < t1; ++t) {
+        if constexpr (DONLY && kDecPairOk<DT, B, RED>) {  // decode-only launches: their own register budget
+          if (t + 1 < t1 && pair_tiles(Jd, t)) {  // two tiles of the run at once (two rANS chains per warp)
+            dec_item2<DT, B>(P, Jd, j, t, smem, S, dec_key);
+            ++t;
+            continue;
+          }
+        }
         if constexpr (RED) {
           if (Jd.nsrc > 1) red_item<DT, B>(P, Jd, j, t, smem, S, dec_key, enc_key, credit_done, ring, pd);
           else dec_item<DT, B, RED>(P, Jd, j, t, smem, S, dec_key, fwd_done);
