@@ -110,6 +110,9 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
 #ifndef UZIP_DEC_NOCLAMP
 #define UZIP_DEC_NOCLAMP 1  // k_decode's staged blocks: no clamp of the word index (1 GiB bf16 0.540 -> 0.524 ms)
 #endif
+#ifndef UZIP_DEC_PTR
+#define UZIP_DEC_PTR 1  // k_decode pairs: word pointers as shared byte addresses updated by IMAD (0.524 -> 0.518 ms)
+#endif
 #ifndef UZIP_STAGE_ASYNC
 #define UZIP_STAGE_ASYNC 1
 #endif
@@ -331,6 +334,11 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
   }
   uint32_t xA = reinterpret_cast<const uint32_t *>(payA)[lane], xB = reinterpret_cast<const uint32_t *>(payB)[lane];
   int32_t pA = (int32_t)KA, pB = (int32_t)KB;
+#if UZIP_DEC_PTR
+  const uint32_t sA0 = (uint32_t)__cvta_generic_to_shared(wA), sB0 = (uint32_t)__cvta_generic_to_shared(wB);
+  uint32_t sA = sA0 + 2u * KA, sB = sB0 + 2u * KB;
+  const uint32_t two = __shfl_sync(0xFFFFFFFFu, 2u, 0);  // 2, opaque to ptxas: keeps the updates IMADs
+#endif
 #pragma unroll 1
   for (int g0 = 0; g0 < kGroups; g0 += kPF) {
 #pragma unroll
@@ -345,13 +353,27 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
         xB = (eB >> 20) * (xB >> kProbBits) + ((eB >> 8) & 0xFFFu);
         const bool nA = xA < kL, nB = xB < kL;
         const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nA), mB = __ballot_sync(0xFFFFFFFFu, nB);
+        uint32_t wa, wb;
+#if UZIP_DEC_PTR
+        if constexpr (NOCLAMP) {
+          // shared-memory byte addresses of the read pointers, updated and offset by IMADs (FMA pipe)
+          // instead of the index add + address IADD3 on the saturated ALU pipe
+          sA -= two * __popc(mA);
+          sB -= two * __popc(mB);
+          const uint32_t aA = sA + two * __popc(mA & lt), aB = sB + two * __popc(mB & lt);
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(wa) : "r"(aA));
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(wb) : "r"(aB));
+        } else
+#endif
+        {
         pA -= __popc(mA);
         pB -= __popc(mB);
         // NOCLAMP (k_decode): a corrupt stream drives p below 0 by at most B words, which stays inside
         // the CTA's shared memory (the payload areas sit above the 17 KB table + offsets); p != 0 at the
         // end reports it.  k_fused's layout clamps.
         const int32_t ia = pA + __popc(mA & lt), ib = pB + __popc(mB & lt);
-        const uint32_t wa = wA[NOCLAMP ? ia : max(ia, 0)], wb = wB[NOCLAMP ? ib : max(ib, 0)];
+        wa = wA[NOCLAMP ? ia : max(ia, 0)], wb = wB[NOCLAMP ? ib : max(ib, 0)];
+        }
         xA = nA ? ((xA << 16) | wa) : xA;
         xB = nB ? ((xB << 16) | wb) : xB;
       }
@@ -386,6 +408,12 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
       __syncwarp();
     }
   }
+#if UZIP_DEC_PTR
+  if constexpr (NOCLAMP) {
+    pA = (int32_t)(sA - sA0) / 2;
+    pB = (int32_t)(sB - sB0) / 2;
+  }
+#endif
   okA = !(pA != 0 || __any_sync(0xFFFFFFFFu, xA != kL));
   okB = !(pB != 0 || __any_sync(0xFFFFFFFFu, xB != kL));
 }

@@ -393,20 +393,34 @@ __device__ __forceinline__ uint32_t symbol_at(const uint8_t *base, uint32_t i) {
 // rcp = 2^32-1 (q = x-1) with the bias raised by M-1.  Entry:
 //   x = rcp, y = f<<19 | shift (renorm threshold + funnel-shift amount),
 //   z = bias, w = M - f.
+#ifndef UZIP_ENC_MULQ
+#define UZIP_ENC_MULQ 0  // A/B: measured slower (0.696 vs 0.679 ms: two IMAD.HI on the chain)
+#endif
+// Encode entry {rcp, y, z, M - f}: floor(x / f) = umulhi(umulhi(x, rcp), y) - d and
+// x' = x + z + q' (M - f) with z = cdf + d (M - f) -- both high multiplies on the FMA pipe
+// (UZIP_ENC_MULQ; y = 2^(32 - sh), or 2^32 - 1 for sh = 0, which undercounts by one).  The
+// renormalization test x >= f << 19 reads M - f (x + (M - f) << 19 >= 2^31).  Without MULQ:
+// y = f << 19 | sh, q = umulhi(x, rcp) >> sh (funnel shift, ALU pipe).
 __host__ __device__ inline uint4 make_enc_entry(uint32_t f, uint32_t cdf) {
   uint4 e;
+  uint32_t sh, d;  // post-shift of the 32-bit reciprocal; undercount of umulhi(x, rcp) against x / f
   if (f < 2) {
-    e.x = 0xFFFFFFFFu;
-    e.y = (f << 19) | 0u;
-    e.z = cdf + kM - 1;
+    e.x = 0xFFFFFFFFu;  // umulhi(x, 2^32 - 1) = x - 1
+    sh = 0, d = 1;
   } else {
     uint32_t s = 0;
     while (f > (1u << s)) ++s;
     e.x = (uint32_t)(((1ull << (s + 31)) + f - 1) / f);
-    e.y = (f << 19) | (s - 1);
-    e.z = cdf;
+    sh = s - 1, d = 0;
+  }
+  if (UZIP_ENC_MULQ) {
+    if (sh == 0) e.y = 0xFFFFFFFFu, d += 1;  // umulhi(t, 2^32 - 1) = t - 1 (t >= 1 here)
+    else e.y = 1u << (32 - sh);
+  } else {
+    e.y = (f << 19) | sh;
   }
   e.w = kM - f;
+  e.z = cdf + d * e.w;
   return e;
 }
 
