@@ -461,7 +461,9 @@ struct FusedCfg {
   // block); f16 and fp8 symbols carry more bits (~2.3-2.8 KB per block on U[-1,1]), so their encode
   // launches park up to 24 KiB -- a tile larger than the ring finishes its look-back before it is stored
   static constexpr int ring(bool red) {
-    return (!red && (DT == kF16 || DT == kE4M3 || DT == kE5M2)) ? UZIP_RING_WIDE : 16384;
+    return red ? 16384
+               : B > 4096 ? 3 * B  // 8192 / 16384-symbol blocks: a coded bf16 tile is ~2.9 / 5.6 KB per block
+               : (DT == kF16 || DT == kE4M3 || DT == kE5M2) ? UZIP_RING_WIDE : 16384;
   }
   static constexpr int kTmaStage = UZIP_ENC_TMA ? B * (int)group_bytes(DT) : 0;  // per warp (A/B only)
   static constexpr int smem(bool dec, bool red) {

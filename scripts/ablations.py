@@ -11,7 +11,8 @@ bytes:
                     chunk -- the paper's "8 MB chunked pipeline" (P:540) / NCCL-slice granularity (P:815);
   * chunked_1MiB    the same at 1 MiB (chunked_64MiB / chunked_256MiB: the rest of BASELINE configs[1]'s
                     pipeline-chunk sweep);
-  * block_1024/2048 the fused path with 1024- / 2048-symbol codec blocks (configs[1]'s block-size sweep);
+  * block_<B>       the fused path with 1024- / 2048- / 8192- / 16384-symbol codec blocks (configs[1]'s
+                    block-size sweep; codec_blocks: the codec alone per B);
   * encode_send     uzip_compress of the whole message, a device copy of the stream (the wire), then
                     uzip_decompress -- serial, no overlap (fig:compare_with_native_pipeline);
   * sm_limited      the fused path with each side's kernel capped at max_ctas CTAs (fig:resource_usage;
@@ -99,7 +100,7 @@ def main():
     p2p_leg("chunked_1MiB", max_ctas=2 * 148, pipe_chunk_bytes=1 << 20)
     for mib in (64, 256):  # BASELINE configs[1] pipeline-chunk sweep (whole slots = "fused" above)
         p2p_leg(f"chunked_{mib}MiB", max_ctas=2 * 148, pipe_chunk_bytes=mib << 20)
-    for bs in (1024, 2048):  # ... and its codec block-size sweep (4096 = "fused")
+    for bs in (1024, 2048, 8192, 16384):  # ... and its codec block-size sweep (4096 = "fused")
         p2p_leg(f"block_{bs}", max_ctas=2 * 148, block_symbols=bs)
     for m in (16, 37, 74, 148):
         p2p_leg(f"sm_limited_{m}ctas", max_ctas=m)
@@ -197,6 +198,30 @@ def codec_legs(uz, x, args, timed, res):
         stream.wait_stream(s2)
     leg("staged_ce_split_send", staged_ce, ref)
     res["codec_legs"] = legs
+    # block-size sweep of the codec alone (configs[1]: B in {1024 ... 16384}): compress and decompress
+    blk = {}
+    y = torch.empty_like(x)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for bs in (1024, 2048, 4096, 8192, 16384):
+        wsb = uz.Workspace(0).get(uz.workspace_bytes(n, uz.BF16, block_symbols=bs), stream)
+        if uz.compress_bound(n, uz.BF16, block_symbols=bs) > out.numel():
+            out = torch.empty(uz.compress_bound(n, uz.BF16, block_symbols=bs), dtype=torch.uint8, device="cuda")
+
+        def comp():
+            with torch.cuda.stream(stream):
+                uz.compress(x, out=out, out_bytes=nb, stream=stream, ws=wsb, block_symbols=bs)
+
+        def dec():
+            with torch.cuda.stream(stream):
+                uz.decompress(out, n, uz.BF16, out=y, status=st, stream=stream, ws=wsb)
+        mc = timed(comp, stream)
+        md = timed(dec, stream)
+        torch.cuda.synchronize()
+        ok = int(st.item()) == 0 and torch.equal(x.view(torch.int16), y.view(torch.int16))
+        blk[f"B{bs}"] = {"compress_ms": round(mc, 4), "decompress_ms": round(md, 4),
+                         "ratio": round(int(nb.item()) / raw, 5), "bit_exact": ok}
+        print("codec_block", bs, blk[f"B{bs}"], flush=True)
+    res["codec_blocks"] = blk
     try:
         res["green_ctx"] = green_ctx_legs(uz, x, args)
     except Exception as e:  # report, do not fail the other legs
