@@ -7,10 +7,11 @@ with it: the C source ``oracle/uzip_oracle.c`` is a plain single-threaded
 restatement of PAPER.md (arxiv 2604.17172) §2.1.2, §3.3
  and §3.4 with the readings listed in DESIGN.md.
 
-Parity unpinned: the exact compressed bytes against the paper's own
-implementation (the paper publishes no format or worked stream; P:168 only
-says the blocks are "merged into a single contiguous output buffer").
-Everything else is pinned by tests/test_oracle_*.py.
+Every function is pinned by tests/test_oracle_*.py and tests/test_golden.py
+(see DESIGN.md "The oracle and its pins").  The UZB1 byte layout is this
+reproduction's definition: the paper publishes no
+format or worked stream (P:168 only says the blocks are "merged into a
+single contiguous output buffer"), so streams are compared GPU vs oracle.
 """
 from __future__ import annotations
 

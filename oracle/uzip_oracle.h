@@ -11,15 +11,22 @@
  * the reading taken is the one listed in DESIGN.md "Readings" (R1..R17,
  * numbered like SURVEY.md 8(c) Q1..Q17).
  *
- * Parity status per function:
- *   uzo_split_elem / uzo_join_elem      pinned (SPEC examples, exhaustive bijection)
- *   uzo_histogram                       pinned (brute force count)
- *   uzo_normalize                       pinned (survey g1/g4 tables)
- *   uzo_encode_block / uzo_decode_block pinned (brute force round trip, information identity)
- *   uzo_compress / uzo_decompress       pinned (round trip, entropy closed forms, size window)
- *   uzo_reduce                          pinned (numpy/torch fp32 fold, special-value table)
- *   exact compressed bytes vs the paper's own implementation: PARITY UNPINNED
- *   (the paper publishes no format or worked stream).
+ * Pins per function (tests/test_oracle_*.py, tests/test_golden.py):
+ *   uzo_split_elem / uzo_join_elem      SPEC S:61-64 examples, exhaustive 2^16 bijections, numpy frexp
+ *                                       fields; fp8 pairs / bytes (R23, R24) exhaustively
+ *   uzo_histogram                       brute-force count (np.bincount)
+ *   uzo_normalize                       S:132-134, invariants, the survey's g1/g4 tables
+ *   uzo_encode_block / uzo_decode_block brute force over all 3^9 lane-0 sequences, information identity,
+ *                                       byte-for-byte the survey's independent g1 prototype (K, sizes,
+ *                                       final states, sha256), stored-raw tie blocks (O7)
+ *   uzo_compress / uzo_decompress       round trips over dtypes x edge sizes, Shannon / N1-cost bounds
+ *                                       from closed-form value distributions, the paper's printed ratios
+ *                                       (Table 1), corrupt-stream errors
+ *   uzo_reduce (sum / min / max)        numpy / torch fp32 folds, special-value tables, permutation
+ *                                       invariance (R11, R25)
+ *   wire streams (oracle/__init__.py)   decode to the plain definitions of the collectives (O13, R26)
+ * The stream layout (UZB1) is this reproduction's definition: the paper prints no
+ * format or worked stream, so bytes are compared GPU-vs-oracle, and the oracle against the pins above.
  */
 #ifndef UZIP_ORACLE_H
 #define UZIP_ORACLE_H
