@@ -89,7 +89,8 @@ __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom 
     join_block<DT, B>(src, in, g, b, dst);  // raw symbols joined straight from the stream
   } else if (size <= (uint32_t)DecShared<DT>::kStage) {
     stage_block(src, size / 16, pay);
-    ok = decode_join_warp<DT, B, UZIP_DEC_NOCLAMP != 0 && DT != kF32>(pay, d, dtab, ring, in, g, b, dst);
+    // (B <= 4096: a corrupt word index reaches at most 8 KiB below the payload, inside the window)
+    ok = decode_join_warp<DT, B, UZIP_DEC_NOCLAMP != 0 && DT != kF32 && B <= 4096>(pay, d, dtab, ring, in, g, b, dst);
   } else {
     // rare: a coded block larger than the staging area is decoded in place from global memory
     // (word indices never leave [0, K), so even a corrupt stream is read in bounds)

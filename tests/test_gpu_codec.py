@@ -379,3 +379,23 @@ def test_unsupported_block_sizes_rejected(uz):
     for B in (512, 3072, 32768):
         with pytest.raises(uz.UzipError):
             uz.compress(x, block_symbols=B)
+
+
+@pytest.mark.parametrize("B", [4096, 16384])
+@pytest.mark.parametrize("dist", ["W", "zeros"])
+def test_garbage_block_states_fail_cleanly(uz, orc, B, dist):
+    """Garbage final lane states make the decoder consume words it does not have (its word index runs
+    below 0; zeros give tiny, smem-staged blocks, W at 16384 large ones decoded in place): k_decode must
+    report a corrupt stream, never fault, and the context stays usable."""
+    n = 12 * B + 5
+    bits = GENS[dist](n, 77, BF16)
+    good = gpu_compress(uz, bits, BF16, block_symbols=B)
+    off_pay = orc.sections(good)["off_pay"]
+    rng = np.random.default_rng(B)
+    for _ in range(3):  # block 0 starts the payload: overwrite its 32 final states with random words
+        bad = bytearray(good)
+        bad[off_pay:off_pay + 128] = rng.integers(0, 256, 128, dtype=np.uint8).tobytes()
+        st, _ = gpu_decompress(uz, bytes(bad), n, BF16)
+        assert st != 0
+    st, back = gpu_decompress(uz, good, n, BF16)
+    assert st == 0 and np.array_equal(back, bits)
