@@ -51,6 +51,12 @@ namespace uzip {
 #ifndef UZIP_DEC_PAIR_MINB
 #define UZIP_DEC_PAIR_MINB 5  // register budget (48); smem holds 4 CTAs
 #endif
+#ifndef UZIP_DEC_PAIR_WIDE
+#define UZIP_DEC_PAIR_WIDE 0  // A/B: f16 / e4m3 pairs too (3 CTAs: f16 U decode 0.156 vs 0.150 ms, e4m3 0.168 vs 0.163)
+#endif
+#ifndef UZIP_DEC_PAIR_STAGE_WIDE
+#define UZIP_DEC_PAIR_STAGE_WIDE 2816
+#endif
 #ifndef UZIP_DEC_PAIR_STAGE
 #define UZIP_DEC_PAIR_STAGE 1664
 #endif
@@ -60,13 +66,17 @@ namespace uzip {
 template <int DT>
 struct DecShared {
   static constexpr bool kExp8 = DT == kBF16;  // 8-bit exponent symbols, one residual plane
-  static constexpr bool kPair = kExp8 && UZIP_DEC_PAIR;  // two blocks per warp (two staging areas)
+  // two blocks per warp (two staging areas): bf16; f16 / e4m3 (one residual byte per symbol, wider
+  // symbols -> larger staging, 3 CTAs) under UZIP_DEC_PAIR_WIDE
+  static constexpr bool kWidePair = UZIP_DEC_PAIR_WIDE && (DT == kF16 || DT == kE4M3);
+  static constexpr bool kPair = (kExp8 || kWidePair) && UZIP_DEC_PAIR;
   static constexpr int kMinB = kPair ? UZIP_DEC_PAIR_MINB : kExp8 ? UZIP_DEC_MINB_EXP8
                               : DT == kF32 ? UZIP_DEC_MINB_F32 : UZIP_DEC_MINB;
   static constexpr int kTab = 4096 * 4;              // decode table
   static constexpr int kSeg = UZIP_DEC_SEG;          // blocks per segment (a multiple of 256)
   static constexpr int kOff = kSeg * 4;              // per-segment block offsets (relative to chunk)
-  static constexpr int kStage = kPair ? UZIP_DEC_PAIR_STAGE : kExp8 ? UZIP_DEC_STAGE_EXP8 : UZIP_DEC_STAGE;  // per block
+  static constexpr int kStage = kWidePair ? UZIP_DEC_PAIR_STAGE_WIDE : kPair ? UZIP_DEC_PAIR_STAGE
+                               : kExp8 ? UZIP_DEC_STAGE_EXP8 : UZIP_DEC_STAGE;  // per block
   static constexpr int kWarpBuf = kStage + 256;      // staged payload + 8-round symbol ring
   static constexpr int kWarpBytes = kWarpBuf * (kPair ? 2 : 1);
   static constexpr int kBytes = kTab + kOff + kWarps * kWarpBytes;
