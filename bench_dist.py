@@ -409,13 +409,39 @@ def run_suites(args, uz, comm, stream, rank, world, local, x, y, role, peer, n):
         ga = torch.Generator(device="cuda")
         ga.manual_seed(3000 + rank)
         scale = torch.exp(torch.randn(4096, device="cuda", generator=ga) * 0.5)
+        # NCCL with its ring algorithm forced as a second baseline (SURVEY 7 hard part 5): NCCL reads
+        # NCCL_ALGO when a communicator is created, so a fresh group is built with the variable set
+        ring_pg, ring_err = None, None
+        if not SMOKE and os.environ.get("UZIP_BENCH_NCCL_RING", "1") != "0":
+            old = os.environ.get("NCCL_ALGO")
+            try:
+                os.environ["NCCL_ALGO"] = "Ring"
+                ring_pg = dist.new_group(backend="nccl")
+                warm = torch.ones(1024, device="cuda")
+                dist.all_reduce(warm, group=ring_pg)  # the communicator is created here
+                torch.cuda.synchronize()
+            except Exception as e:  # report, keep the suite
+                ring_pg, ring_err = None, repr(e)[:200]
+            finally:
+                if old is None:
+                    os.environ.pop("NCCL_ALGO", None)
+                else:
+                    os.environ["NCCL_ALGO"] = old
         for k in ks:
             T = 32 << k
             a = (torch.randn(T, 4096, device="cuda", generator=ga) * scale).to(torch.bfloat16)
             o = torch.empty_like(a)
             nb = a.clone()
-            res[f"{2 * a.numel() >> 10}KiB"] = pair(lambda: comm.all_reduce(o, a, stream),
-                                                     lambda: dist.all_reduce(nb), 2 * a.numel())
+            key = f"{2 * a.numel() >> 10}KiB"
+            res[key] = pair(lambda: comm.all_reduce(o, a, stream), lambda: dist.all_reduce(nb), 2 * a.numel())
+            if ring_pg is not None:
+                try:
+                    mr = timed(in_stream(lambda: dist.all_reduce(nb, group=ring_pg)))
+                    res[key]["nccl_ring_GBps"] = gbs(2 * a.numel(), mr)
+                except Exception as e:
+                    res[key]["nccl_ring_error"] = repr(e)[:200]
+        if ring_err:
+            res["nccl_ring_error"] = ring_err
         return res
 
     def c5_ag_rs():
