@@ -290,8 +290,12 @@ void dec_job(uzip_comm *c, Plan &p, int j, int dt, uint64_t n, bool compressed, 
   // more sources the table changes with every source of a tile anyway, so they keep single tiles.
   J.run = 1;
   const int remote = (int)J.nsrc - (me_idx >= 0 ? 1 : 0);
-  if (compressed && remote == 1)
+  if (compressed && remote == 1) {
     J.run = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(UZIP_DEC_RUN_MAX, J.ntiles / 1024));
+    // UZIP_DEC_RUN forces the run length (tests: paired-tile D items on small messages)
+    static const int forced = getenv("UZIP_DEC_RUN") ? atoi(getenv("UZIP_DEC_RUN")) : 0;
+    if (forced > 0) J.run = (uint32_t)forced;
+  }
   p.nd_jobs = j + 1;
 }
 

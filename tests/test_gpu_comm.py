@@ -851,3 +851,25 @@ def test_large_blocks_p2p_allgather(uz, orc, B):
             g.comms[0].all_reduce(outs[0], outs[0])
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("dtype", [BF16, F16, F32])
+@pytest.mark.parametrize("codec", [dict(), dict(chunk_blocks=16)])
+def test_paired_tile_receiver_small(uz, orc, dtype, codec):
+    """Decode-only receivers pair consecutive tiles of a run (two rANS chains per warp).  Runs only
+    form on >= 128 MiB rounds by default, so UZIP_DEC_RUN (read once per process: see
+    test_paired_tile_receiver_forced_runs) forces them; here: whatever the run length, a message with
+    incompressible blocks, several chunks and a ragged tail arrives bit-exact with the oracle's stream."""
+    g = Group(uz, 2, staging_bytes=64 << 20, min_compress_bytes=1, **codec)
+    try:
+        n = 41 * 8 * 4096 + 4096 * 3 + 7
+        bits = gen("W", n, 606 + dtype, dtype)
+        bits[4096 * 50:4096 * 53] = synth.random_bits(4096 * 3, 9, dtype)  # stored-raw blocks
+        x = dev(bits, dtype)
+        y = torch.empty_like(x)
+        g.run(lambda r, c, s: c.send(x, 1, s) if r == 0 else c.recv(y, 0, s))
+        assert np.array_equal(host(y, dtype), bits)
+        ref = orc.compress(dtype, bits, **codec)
+        assert g.comms[1].read_staging(0, 0, len(ref)) == ref
+    finally:
+        g.close()

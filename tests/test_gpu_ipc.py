@@ -116,3 +116,16 @@ def test_tile_trace_shows_overlap():
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["tiles"] > 100 and res["receiver_tiles_done_before_sender_finished"] > 0.25
     assert res["allreduce_one_pass"]["ag_tiles_released_before_last_reduced_tile"] > 0.25
+
+
+def test_paired_tile_receiver_forced_runs():
+    """Paired-tile D items (decode-only receivers, runs of consecutive tiles) on small messages:
+    UZIP_DEC_RUN=4 forces runs, so test_paired_tile_receiver_small pairs tiles (bf16 / f16 pairs, fp32
+    one by one; chunk boundaries and raw blocks break pairs)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, UZIP_DEC_RUN="4")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_comm.py"), "-k", "paired_tile_receiver_small or p2p_bit_exact"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
