@@ -113,6 +113,15 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
 #ifndef UZIP_DEC_PTR
 #define UZIP_DEC_PTR 1  // k_decode pairs: word pointers as shared byte addresses updated by IMAD (0.524 -> 0.518 ms)
 #endif
+#ifndef UZIP_DEC_GE
+#define UZIP_DEC_GE 1  // pairs: read address = s - 2*popc(m & lanemask_ge), both IMADs off the old s (no negation MOV)
+#endif
+#ifndef UZIP_DEC_TADDR
+#define UZIP_DEC_TADDR 0  // A/B: table address as LOP3 + IMAD
+#endif
+#ifndef UZIP_DEC_HI
+#define UZIP_DEC_HI 0  // A/B: the state update's shifts as high multiplies (FMA pipe)
+#endif
 #ifndef UZIP_STAGE_ASYNC
 #define UZIP_STAGE_ASYNC 1
 #endif
@@ -337,7 +346,20 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
 #if UZIP_DEC_PTR
   const uint32_t sA0 = (uint32_t)__cvta_generic_to_shared(wA), sB0 = (uint32_t)__cvta_generic_to_shared(wB);
   uint32_t sA = sA0 + 2u * KA, sB = sB0 + 2u * KB;
-  const uint32_t two = __shfl_sync(0xFFFFFFFFu, 2u, 0);  // 2, opaque to ptxas: keeps the updates IMADs
+  const uint32_t two = __shfl_sync(0xFFFFFFFFu, UZIP_DEC_GE ? 0xFFFFFFFEu : 2u, 0);  // +-2, opaque to ptxas: keeps the updates IMADs
+#if UZIP_DEC_GE
+  const uint32_t ge = ~lt;
+#endif
+#endif
+#if UZIP_DEC_TADDR
+  const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(dtab);
+  const uint32_t four = __shfl_sync(0xFFFFFFFFu, 4u, 0);  // opaque: the index scaling stays one IMAD
+#endif
+#if UZIP_DEC_HI
+  // opaque 2^20 / 2^12 / -4096: x >> 12 = hi(x * 2^20), freq = e >> 20 = hi(e * 2^12); with e >> 8 = freq << 12 | bias,
+  // x' = freq * (x >> 12) + bias = freq * ((x >> 12) - 4096) + (e >> 8)  (mod 2^32)
+  const uint32_t k20 = __shfl_sync(0xFFFFFFFFu, 1u << 20, 0), k12 = __shfl_sync(0xFFFFFFFFu, 1u << 12, 0);
+  const uint32_t m4096 = __shfl_sync(0xFFFFFFFFu, 0u - 4096u, 0);
 #endif
 #pragma unroll 1
   for (int g0 = 0; g0 < kGroups; g0 += kPF) {
@@ -345,12 +367,41 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
     for (int q = 0; q < kPF; ++q) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
+#if UZIP_DEC_TADDR
+        // table byte address = (x & 4095) * 4 + base as LOP3 + IMAD: two ops between x and the lookup
+        // (ptxas emitted IMAD.SHL + LOP3 + IADD)
+        uint32_t eA, eB;
+        asm("{\n\t.reg .b32 i, a;\n\tand.b32 i, %1, 4095;\n\tmad.lo.u32 a, i, %2, %3;\n\tld.shared.u32 %0, [a];\n\t}"
+            : "=r"(eA) : "r"(xA), "r"(four), "r"(tbase));
+        asm("{\n\t.reg .b32 i, a;\n\tand.b32 i, %1, 4095;\n\tmad.lo.u32 a, i, %2, %3;\n\tld.shared.u32 %0, [a];\n\t}"
+            : "=r"(eB) : "r"(xB), "r"(four), "r"(tbase));
+#else
         const uint32_t eA = dtab[xA & (kM - 1)];
         const uint32_t eB = dtab[xB & (kM - 1)];
+#endif
         ringA[u * 32 + lane] = (uint8_t)eA;
         ringB[u * 32 + lane] = (uint8_t)eB;
+#if UZIP_DEC_HI
+        {
+#if UZIP_DEC_HI == 1
+          uint32_t hA, hB;
+          asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(hA) : "r"(xA), "r"(k20), "r"(m4096));
+          asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(hB) : "r"(xB), "r"(k20), "r"(m4096));
+          xA = __umulhi(eA, k12) * hA + (eA >> 8);
+          xB = __umulhi(eB, k12) * hB + (eB >> 8);
+#elif UZIP_DEC_HI == 2
+          xA = __umulhi(eA, k12) * __umulhi(xA, k20) + ((eA >> 8) & 0xFFFu);
+          xB = __umulhi(eB, k12) * __umulhi(xB, k20) + ((eB >> 8) & 0xFFFu);
+#else
+          const uint32_t fA = __umulhi(eA, k12), fB = __umulhi(eB, k12);
+          xA = fA * __umulhi(xA, k20) + (fA * m4096 + (eA >> 8));
+          xB = fB * __umulhi(xB, k20) + (fB * m4096 + (eB >> 8));
+#endif
+        }
+#else
         xA = (eA >> 20) * (xA >> kProbBits) + ((eA >> 8) & 0xFFFu);
         xB = (eB >> 20) * (xB >> kProbBits) + ((eB >> 8) & 0xFFFu);
+#endif
         const bool nA = xA < kL, nB = xB < kL;
         const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nA), mB = __ballot_sync(0xFFFFFFFFu, nB);
         uint32_t wa, wb;
@@ -358,9 +409,17 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
         if constexpr (NOCLAMP) {
           // shared-memory byte addresses of the read pointers, updated and offset by IMADs (FMA pipe)
           // instead of the index add + address IADD3 on the saturated ALU pipe
+#if UZIP_DEC_GE
+          // the k renormalizing lanes read the last k unread words: lane l's word sits popc(m & ge_l) words
+          // below the old pointer (two = -2 here); both IMADs read the old pointer
+          const uint32_t aA = sA + two * __popc(mA & ge), aB = sB + two * __popc(mB & ge);
+          sA += two * __popc(mA);
+          sB += two * __popc(mB);
+#else
           sA -= two * __popc(mA);
           sB -= two * __popc(mB);
           const uint32_t aA = sA + two * __popc(mA & lt), aB = sB + two * __popc(mB & lt);
+#endif
           asm volatile("ld.shared.u16 %0, [%1];" : "=r"(wa) : "r"(aA));
           asm volatile("ld.shared.u16 %0, [%1];" : "=r"(wb) : "r"(aB));
         } else
