@@ -31,6 +31,9 @@
 #include "uzip_internal.h"
 
 // Tuning knobs (defaults measured best on B200; overridable for experiments with -D)
+#ifndef UZIP_ENC_PIPE
+#define UZIP_ENC_PIPE 0  // A/B: rounds per software-pipelined load group (0: UZIP_ENC_GROUP groups, loaded in place)
+#endif
 #ifndef UZIP_ENC_GROUP
 #define UZIP_ENC_GROUP 8  // encoder rounds whose symbols/table entries are loaded ahead (r02b: 8 beats 4, 0.668 vs 0.676 ms)
 #endif
@@ -693,6 +696,64 @@ __device__ __forceinline__ void encode_block(const EncJob &J, const StreamGeom &
   const uint32_t spare = (uint32_t)B / 2 + (uint32_t)lane;
   uint32_t dw = 0, didx = spare;
   constexpr uint32_t kCap = B / 2 - 64;  // words that fit before the raw threshold
+#if UZIP_ENC_PIPE
+  if (!GLOBAL) {
+    // software-pipelined groups of kH rounds: the next group's symbols and table entries are loaded
+    // while this group codes (two register sets of kH entries), so the symbol -> entry load chain is
+    // off the state chain except for the first group.  Words stay below the end of the coding group's
+    // rows (lim), so the prefetched rows are never overwritten before they are read.
+    constexpr int kH = UZIP_ENC_PIPE;
+    constexpr int kNH = C::kRounds / kH;
+    static_assert(kNH % 2 == 0, "pipelined encoder: an even number of groups");
+    uint4 ea[kH], eb[kH];
+    auto load = [&](uint4 *e, int h) {
+#pragma unroll
+      for (int u = 0; u < kH; ++u) e[u] = tab[buf[(kH * h + u) * 32 + lane]];
+    };
+    auto code = [&](const uint4 *ent, int h) {
+      const uint32_t lim = min(kCap, (uint32_t)(16 * kH) * (h + 1));
+#pragma unroll
+      for (int u = 0; u < kH; ++u) {
+        const uint4 e = ent[u];
+        const uint32_t tt = x + e.w * (1u << 19);
+        uint32_t m, nidx;
+        buf16[didx] = (uint16_t)dw;
+        dw = x;
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 r, c;\n\t"
+            "setp.lt.s32 q, %3, 0;\n\t"
+            "vote.sync.ballot.b32 %0, q, -1;\n\t"
+            "and.b32 r, %0, %4;\n\t"
+            "popc.b32 c, r;\n\t"
+            "add.u32 r, %5, c;\n\t"
+            "min.u32 r, r, %6;\n\t"
+            "selp.b32 %1, r, %7, q;\n\t"
+            "@q shr.b32 %2, %2, 16;\n\t}"
+            : "=r"(m), "=r"(nidx), "+r"(x)
+            : "r"(tt), "r"(lt), "r"(wp), "r"(lim - 1), "r"(spare));
+        didx = nidx;
+        wp += __popc(m);
+        const uint32_t q = __funnelshift_r(__umulhi(x, e.x), 0u, e.y);
+        x = x + e.z + q * e.w;
+      }
+      over |= wp > lim;
+    };
+    load(ea, 0);
+#pragma unroll 1
+    for (int h = 0; h < kNH; h += 2) {
+      __syncwarp();  // every lane read rows h, h+1 before words may land in them
+      load(eb, h + 1);
+      code(ea, h);
+      __syncwarp();
+      if (h + 2 < kNH) load(ea, h + 2);
+      code(eb, h + 1);
+    }
+    buf16[didx] = (uint16_t)dw;
+    x_out = x;
+    K = wp;
+    ovf = over;
+    return;
+  }
+#endif
   constexpr int kG = UZIP_ENC_GROUP;
 #pragma unroll 1
   for (int G = 0; G < C::kRounds / kG; ++G) {
