@@ -116,6 +116,9 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
 #ifndef UZIP_DEC_GE
 #define UZIP_DEC_GE 1  // pairs: read address = s - 2*popc(m & lanemask_ge), both IMADs off the old s (no negation MOV)
 #endif
+#ifndef UZIP_DEC_RING16
+#define UZIP_DEC_RING16 0  // A/B: pairs store both chains' symbols of a round with one 16-bit store
+#endif
 #ifndef UZIP_DEC_TADDR
 #define UZIP_DEC_TADDR 0  // A/B: table address as LOP3 + IMAD
 #endif
@@ -379,8 +382,14 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
         const uint32_t eA = dtab[xA & (kM - 1)];
         const uint32_t eB = dtab[xB & (kM - 1)];
 #endif
+#if UZIP_DEC_RING16
+        // both chains' symbols of this round in one 16-bit store (rounds 0-3 in ringA, 4-7 in ringB)
+        *reinterpret_cast<uint16_t *>((u < 4 ? ringA : ringB) + ((u & 3) * 32 + lane) * 2) =
+            (uint16_t)__byte_perm(eA, eB, 0x0040);
+#else
         ringA[u * 32 + lane] = (uint8_t)eA;
         ringB[u * 32 + lane] = (uint8_t)eB;
+#endif
 #if UZIP_DEC_HI
         {
 #if UZIP_DEC_HI == 1
@@ -439,8 +448,15 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
       __syncwarp();
       const int gi = g0 + q;
       const uint32_t e0 = 256 * gi + 8 * lane;
+#if UZIP_DEC_RING16
+      // elements 8 lane .. 8 lane + 7 = round lane / 4, lanes 8 (lane % 4) ..: 16 bytes, A and B interleaved
+      const uint4 v16 = *reinterpret_cast<const uint4 *>((lane < 16 ? ringA : ringB) + (lane & 15) * 16);
+      const uint2 sA = make_uint2(__byte_perm(v16.x, v16.y, 0x6420), __byte_perm(v16.z, v16.w, 0x6420));
+      const uint2 sB = make_uint2(__byte_perm(v16.x, v16.y, 0x7531), __byte_perm(v16.z, v16.w, 0x7531));
+#else
       const uint2 sA = *reinterpret_cast<const uint2 *>(ringA + 8 * lane);
       const uint2 sB = *reinterpret_cast<const uint2 *>(ringB + 8 * lane);
+#endif
       uint4 vA, vB;
       if (DT == kBF16) {
         join4_bf16(sA.x, rA[q].x, vA.x, vA.y);
