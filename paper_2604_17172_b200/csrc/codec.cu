@@ -39,9 +39,10 @@ namespace uzip {
 #endif
 // bf16 warps decode two coded blocks at once, their rANS chains interleaved (decode_join_warp2): the
 // decoder is latency-bound on its lookup -> renormalize -> word-fetch chain, and a second chain per
-// warp hides it better than more warps can (smem holds 4 CTAs x 8 warps x 2 chains at 1664 staged
-// bytes per block, 48 registers): 1 GiB bf16 decode 0.565 -> 0.540 ms.  Raw, oversized or lone
-// blocks take the one-chain path.
+// warp hides it better than more warps can (48 registers): 1 GiB bf16 decode 0.565 -> 0.540 ms.  Raw,
+// oversized or lone blocks take the one-chain path.  Staging 1488 bytes per block (W = bf16 N(0, 0.02)
+// blocks code to 1408-1488 bytes; a larger one takes the one-chain path) fits 5 CTAs x 8 warps x 2 chains
+// per SM (45.3 KB each; 1664 bytes held 4): 0.511 -> 0.501 ms.
 #ifndef UZIP_DEC_PAIR
 #define UZIP_DEC_PAIR 1
 #endif
@@ -57,8 +58,11 @@ namespace uzip {
 #ifndef UZIP_DEC_PAIR_STAGE_WIDE
 #define UZIP_DEC_PAIR_STAGE_WIDE 2816
 #endif
+#ifndef UZIP_DEC_CARVEOUT
+#define UZIP_DEC_CARVEOUT 0  // A/B: preferred shared-memory carveout (percent) of k_decode; 0 = driver default
+#endif
 #ifndef UZIP_DEC_PAIR_STAGE
-#define UZIP_DEC_PAIR_STAGE 1664
+#define UZIP_DEC_PAIR_STAGE 1488  // 5 CTAs x 8 warps x 2 chains (45.3 KB per CTA); 1664 held 4: 0.511 -> 0.501 ms
 #endif
 #ifndef UZIP_DEC_SEG
 #define UZIP_DEC_SEG 256
@@ -378,6 +382,9 @@ cudaError_t launch_decode_t(const void *in, uint64_t in_bytes, void *out, uint64
   if (!attr[dev]) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecShared<DT>::kBytes);
     if (e != cudaSuccess) return e;
+#if UZIP_DEC_CARVEOUT
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, UZIP_DEC_CARVEOUT);
+#endif
     attr[dev] = true;
   }
   int grid = sm_count() * occupancy(kern, 256, DecShared<DT>::kBytes);
