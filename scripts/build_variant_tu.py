@@ -27,6 +27,9 @@ for src in _build.sources():
     if base in tus:
         obj = os.path.join(vdir, base + ".o")
         cmd = [_build.NVCC, *_build.FLAGS, *[f"-D{d}" for d in defines], "-c", "-o", obj, src]
+        dflt = os.path.join(cache, base + ".o")  # keep the default cache complete (a later default link)
+        if not (os.path.exists(dflt) and os.path.getmtime(dflt) > newest_dep):
+            procs.append((subprocess.Popen([_build.NVCC, *_build.FLAGS, "-c", "-o", dflt, src]), None))
     else:
         obj = os.path.join(cache, base + ".o")
         if os.path.exists(obj) and os.path.getmtime(obj) > newest_dep:
@@ -36,7 +39,7 @@ for src in _build.sources():
     objs.append(obj)
     procs.append((subprocess.Popen(cmd), cmd))
 for p, cmd in procs:
-    if p.wait() != 0:
+    if p.wait() != 0 and cmd is not None:
         raise subprocess.CalledProcessError(p.returncode, cmd)
 lib = os.path.join(out_dir, name + ".so")
 subprocess.check_call([_build.NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs])
