@@ -399,3 +399,27 @@ def test_garbage_block_states_fail_cleanly(uz, orc, B, dist):
         assert st != 0
     st, back = gpu_decompress(uz, good, n, BF16)
     assert st == 0 and np.array_equal(back, bits)
+
+
+def test_pair_staging_boundary_mixed_blocks(uz, orc):
+    """k_decode pairs two coded bf16 blocks per warp when both fit its 1488-byte staging areas; a pair
+    with an oversized block falls back to one chain per block.  Blocks here code to 1472-1744 bytes
+    (W blocks next to blocks with 15 % U[-1,1] elements, one shared chunk table), so pairs of both kinds
+    and a lone last block (65 blocks) occur.  Stream == oracle, round trip exact."""
+    B, nb = 4096, 65
+    bits = synth.normal(nb * B, 0.02, 501)
+    u = synth.uniform(nb * B, 502)
+    rng = np.random.default_rng(7)
+    for i in np.nonzero(rng.random(nb) < 0.5)[0]:
+        m = rng.random(B) < 0.15
+        blk = bits[i * B:(i + 1) * B]
+        blk[m] = u[i * B:(i + 1) * B][m]
+    ref = orc.compress(BF16, bits)
+    sec = orc.sections(ref)
+    k = np.frombuffer(ref[sec["off_dir"]:sec["off_dir"] + 4 * nb], dtype=np.uint32).astype(np.int64)
+    size = (128 + 2 * k + 15) // 16 * 16
+    assert (size <= 1488).sum() >= 4 and (size > 1488).sum() >= 4 and size.max() < B
+    got = gpu_compress(uz, bits, BF16)
+    assert got == ref
+    st, back = gpu_decompress(uz, got, bits.size, BF16)
+    assert st == 0 and np.array_equal(back, bits)
