@@ -342,9 +342,9 @@ def run_codec(args):
         "data": "synthetic", "config": config_for(args),
         "compression_ratio": round(r, 5),
         "encode": {"ms": round(enc_ms, 4), "uncompressed_GBps": round(raw / (enc_ms / 1e3) / GB, 2),
-                   "hbm_GBps": round(enc_gbs, 1)},
+                   "hbm_GBps": round(enc_gbs, 1), "hbm_frac": round(enc_gbs / hbm, 4)},
         "decode": {"ms": round(dec_ms, 4), "uncompressed_GBps": round(raw / (dec_ms / 1e3) / GB, 2),
-                   "hbm_GBps": round(dec_gbs, 1)},
+                   "hbm_GBps": round(dec_gbs, 1), "hbm_frac": round(dec_gbs / hbm, 4)},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": round(dom[1], 1), "peak": hbm,
                      "peak_source": src, "unit": "GB/s", "frac": round(dom[1] / hbm, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom[2]},
