@@ -116,6 +116,9 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
 #ifndef UZIP_DEC_GE
 #define UZIP_DEC_GE 1  // pairs: read address = s - 2*popc(m & lanemask_ge), both IMADs off the old s (no negation MOV)
 #endif
+#ifndef UZIP_DEC_PTRC
+#define UZIP_DEC_PTRC 0  // A/B: the clamped pairs (k_fused receivers) use the pointer form too, clamped at word 0
+#endif
 #ifndef UZIP_DEC_RING16
 #define UZIP_DEC_RING16 0  // A/B: pairs store both chains' symbols of a round with one 16-bit store
 #endif
@@ -415,19 +418,27 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
         const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nA), mB = __ballot_sync(0xFFFFFFFFu, nB);
         uint32_t wa, wb;
 #if UZIP_DEC_PTR
-        if constexpr (NOCLAMP) {
+        if constexpr (NOCLAMP || UZIP_DEC_PTRC) {
           // shared-memory byte addresses of the read pointers, updated and offset by IMADs (FMA pipe)
           // instead of the index add + address IADD3 on the saturated ALU pipe
 #if UZIP_DEC_GE
           // the k renormalizing lanes read the last k unread words: lane l's word sits popc(m & ge_l) words
           // below the old pointer (two = -2 here); both IMADs read the old pointer
-          const uint32_t aA = sA + two * __popc(mA & ge), aB = sB + two * __popc(mB & ge);
+          uint32_t aA = sA + two * __popc(mA & ge), aB = sB + two * __popc(mB & ge);
+          if constexpr (!NOCLAMP) {  // k_fused's layout: a corrupt stream's reads stop at word 0
+            aA = (uint32_t)max((int32_t)aA, (int32_t)sA0);
+            aB = (uint32_t)max((int32_t)aB, (int32_t)sB0);
+          }
           sA += two * __popc(mA);
           sB += two * __popc(mB);
 #else
           sA -= two * __popc(mA);
           sB -= two * __popc(mB);
-          const uint32_t aA = sA + two * __popc(mA & lt), aB = sB + two * __popc(mB & lt);
+          uint32_t aA = sA + two * __popc(mA & lt), aB = sB + two * __popc(mB & lt);
+          if constexpr (!NOCLAMP) {
+            aA = (uint32_t)max((int32_t)aA, (int32_t)sA0);
+            aB = (uint32_t)max((int32_t)aB, (int32_t)sB0);
+          }
 #endif
           asm volatile("ld.shared.u16 %0, [%1];" : "=r"(wa) : "r"(aA));
           asm volatile("ld.shared.u16 %0, [%1];" : "=r"(wb) : "r"(aB));
@@ -484,7 +495,7 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
     }
   }
 #if UZIP_DEC_PTR
-  if constexpr (NOCLAMP) {
+  if constexpr (NOCLAMP || UZIP_DEC_PTRC) {
     pA = (int32_t)(sA - sA0) / 2;
     pB = (int32_t)(sB - sB0) / 2;
   }
