@@ -116,6 +116,9 @@ __device__ __forceinline__ bool build_dtab(const uint16_t *ft, uint32_t *dtab, u
 #ifndef UZIP_DEC_GE
 #define UZIP_DEC_GE 1  // pairs: read address = s - 2*popc(m & lanemask_ge), both IMADs off the old s (no negation MOV)
 #endif
+#ifndef UZIP_DEC_PAIR_PF
+#define UZIP_DEC_PAIR_PF 2  // pairs: residual prefetch distance in 8-round groups
+#endif
 #ifndef UZIP_DEC_PTRC
 #define UZIP_DEC_PTRC 0  // A/B: the clamped pairs (k_fused receivers) use the pointer form too, clamped at word 0
 #endif
@@ -334,7 +337,7 @@ __device__ __forceinline__ void decode_join_warp2(const uint8_t *payA, uint32_t 
                                                   uint64_t bB, uint8_t *dstA, uint8_t *dstB, bool &okA, bool &okB) {
   static_assert(DT == kBF16 || DT == kF16 || DT == kE4M3, "one residual byte per symbol");
   constexpr int kGroups = B / 256;
-  constexpr int kPF = 2;  // residual prefetch distance in groups, per block (1 / 4: 0.542 / 0.553 vs 0.540 ms)
+  constexpr int kPF = UZIP_DEC_PAIR_PF;  // residual prefetch distance in groups, per block (1 / 4: 0.542 / 0.553 vs 0.540 ms at 4 CTAs)
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   const uint16_t *wA = reinterpret_cast<const uint16_t *>(payA) + 64;
