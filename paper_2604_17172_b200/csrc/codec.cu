@@ -82,6 +82,9 @@ struct DecShared {
   static constexpr int kStage = kWidePair ? UZIP_DEC_PAIR_STAGE_WIDE : kPair ? UZIP_DEC_PAIR_STAGE
                                : kExp8 ? UZIP_DEC_STAGE_EXP8 : UZIP_DEC_STAGE;  // per block
   static constexpr int kWarpBuf = kStage + 256;      // staged payload + 8-round symbol ring
+  // one-chain decodes (raw neighbours, oversized or lone blocks) of pair launches stage into the whole
+  // warp buffer (both pair areas, one ring at its end): blocks up to 3232 bytes stay in smem
+  static constexpr int kStage1 = (kPair ? 2 : 1) * kWarpBuf - 256;
   static constexpr int kWarpBytes = kWarpBuf * (kPair ? 2 : 1);
   static constexpr int kBytes = kTab + kOff + kWarps * kWarpBytes;
   static_assert(kStage % 16 == 0 && kSeg % 256 == 0, "decoder smem layout");
@@ -101,7 +104,7 @@ __device__ void decode_block_t(const uint8_t *__restrict__ in, const StreamGeom 
   bool ok = true;
   if (d == kRawBlock) {
     join_block<DT, B>(src, in, g, b, dst);  // raw symbols joined straight from the stream
-  } else if (size <= (uint32_t)DecShared<DT>::kStage) {
+  } else if (size <= (uint32_t)DecShared<DT>::kStage1) {
     stage_block(src, size / 16, pay);
     // (B <= 4096: a corrupt word index reaches at most 8 KiB below the payload, inside the window)
     ok = decode_join_warp<DT, B, UZIP_DEC_NOCLAMP != 0 && DT != kF32 && B <= 4096>(pay, d, dtab, ring, in, g, b, dst);
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(256, DecShared<DT>::kMinB) k_decode(const uint
   uint32_t *soff = reinterpret_cast<uint32_t *>(smem + DS::kTab);
   const int tid = threadIdx.x, lane = tid & 31, warp = warp_id();
   uint8_t *pay = smem + DS::kTab + DS::kOff + warp * DS::kWarpBytes;
-  uint8_t *ring = pay + DS::kStage;
+  uint8_t *ring = pay + DS::kStage1;  // the one-chain ring (pairs use their own two)
 
   __shared__ uint32_t s_red[kWarps];
   __shared__ uint32_t s_bad;
