@@ -312,7 +312,7 @@ def run_codec(args):
     dec_bytes = total + raw           # read stream, write output
     enc_gbs = enc_bytes / (enc_ms / 1e3) / GB
     dec_gbs = dec_bytes / (dec_ms / 1e3) / GB
-    dom = ("k_hist+k_norm+k_fused (uzip_compress)", enc_gbs, enc_bytes) if enc_ms >= dec_ms else \
+    dom = ("k_fused (uzip_compress; tables by its T items)", enc_gbs, enc_bytes) if enc_ms >= dec_ms else \
         ("k_decode (uzip_decompress)", dec_gbs, dec_bytes)
     traffic = ncu_traffic(["k_hist", "k_norm", "k_fused"] if enc_ms >= dec_ms else ["k_decode"], args.bytes)
 
@@ -363,13 +363,10 @@ def run_codec(args):
 
 
 def launches_per_roundtrip(nbytes: int) -> int:
-    """Our kernels per compress + decompress of a bf16 message: k_fused + k_decode, plus k_hist and
-    k_norm for streams of >= 16 table chunks (csrc/uzip_internal.h kTableKernelChunks; smaller ones
-    build their tables with T items inside k_fused); UZIP_TABLE_KERNELS=1/0 forces either."""
-    v = os.environ.get("UZIP_TABLE_KERNELS")
-    chunks = -(-nbytes // (8 << 20))
-    kernels = (v != "0") if v is not None else chunks >= 16
-    return 4 if kernels else 2
+    """Our kernels per compress + decompress of a bf16 message: k_fused (its T items build the tables,
+    csrc/api.cu table_kernels) + k_decode; UZIP_TABLE_KERNELS=1 adds the k_hist and k_norm launches."""
+    del nbytes
+    return 4 if os.environ.get("UZIP_TABLE_KERNELS", "0") != "0" else 2
 
 
 def run_c1(uz, reps: int = 200):

@@ -12,14 +12,15 @@ using namespace uzip;
 
 namespace uzip {
 
-bool table_kernels(uint64_t n_chunks) {
-  // UZIP_TABLE_KERNELS=1 / 0 forces the two table launches / the T items.  By default small streams
-  // (< kTableKernelChunks chunks) use T items, which save two dependent launches (C1 4 MiB compress:
-  // 25 vs 33 us), and large ones the launches, which spare every E item the table-flag poll (1 GiB
-  // codec: equal, 0.7265 ms either way; loopback 1 GiB P2P: 2.15 vs 2.37 ms).
+bool table_kernels(uint64_t n_chunks, bool codec) {
+  // UZIP_TABLE_KERNELS=1 / 0 forces the two table launches / the T items.  By default the codec call
+  // (uzip_compress) always builds its tables with T items inside its one k_fused launch (C1 4 MiB
+  // compress: 25 vs 33 us; 1 GiB: 0.661 vs 0.666 ms), and communication launches do so for small
+  // streams (< kTableKernelChunks chunks) only: large ones launch k_hist + k_norm ahead, which overlap
+  // the slot-credit wait and spare every E item the table-flag poll (loopback 1 GiB P2P: 2.15 vs 2.37 ms).
   static const int v = getenv("UZIP_TABLE_KERNELS") ? atoi(getenv("UZIP_TABLE_KERNELS")) : -1;
   if (v >= 0) return v != 0;
-  return n_chunks >= kTableKernelChunks;
+  return !codec && n_chunks >= kTableKernelChunks;
 }
 
 uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g) {
@@ -110,7 +111,7 @@ uzip_status_t uzip_compress(const void *in, size_t count, uzip_dtype_t dtype, vo
   p.epoch = reinterpret_cast<uint32_t *>(w + 28);
   cudaStream_t cs = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  if (table_kernels(J.g.n_chunks)) {  // large streams: k_hist + k_norm launches
+  if (table_kernels(J.g.n_chunks, true)) {  // forced by UZIP_TABLE_KERNELS=1: k_hist + k_norm launches
     e = launch_tables((int)dtype, p, cs);
     p.tables_ready = 1;
   } else {

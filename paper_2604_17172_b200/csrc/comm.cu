@@ -353,7 +353,7 @@ uzip_status_t launch(uzip_comm *c, Plan &p, bool compressed, cudaStream_t st) {
   if (compressed && p.ne > 0) {
     uint64_t chunks = 0;
     for (int j = 0; j < p.ne; ++j) chunks = std::max<uint64_t>(chunks, p.e[j].raw ? 0 : p.e[j].g.n_chunks);
-    if (table_kernels(chunks)) {
+    if (table_kernels(chunks, false)) {
       if (launch_tables(p.dtype, p, st) != cudaSuccess) return UZIP_ERR_CUDA;
       p.tables_ready = 1;
     } else {

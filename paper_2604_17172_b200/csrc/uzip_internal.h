@@ -23,9 +23,10 @@ cudaError_t launch_decompress(int dtype, const void *in, uint64_t in_bytes, void
 uzip_status_t resolve_geom(int dtype, uint64_t n, const uzip_codec_params_t *p, StreamGeom *g);
 
 // Whether a launch whose largest encode stream has n_chunks table chunks builds its tables with
-// the k_hist + k_norm launches (true) or with T items inside k_fused (false); UZIP_TABLE_KERNELS
-// overrides (A/B of the single-kernel table build).
+// the k_hist + k_norm launches (true) or with T items inside k_fused (false): the codec call always
+// uses T items, communication launches from kTableKernelChunks chunks on use the launches;
+// UZIP_TABLE_KERNELS overrides (A/B of the single-kernel table build).
 constexpr uint64_t kTableKernelChunks = 16;  // >= 128 MiB of 2-byte input per stream
-bool table_kernels(uint64_t n_chunks);
+bool table_kernels(uint64_t n_chunks, bool codec);
 
 }  // namespace uzip
