@@ -58,6 +58,9 @@ namespace uzip {
 #ifndef UZIP_DEC_PAIR_STAGE_WIDE
 #define UZIP_DEC_PAIR_STAGE_WIDE 2816
 #endif
+#ifndef UZIP_DEC_L2PF
+#define UZIP_DEC_L2PF 0  // A/B: L2 prefetch of the next pair's payload
+#endif
 #ifndef UZIP_DEC_CARVEOUT
 #define UZIP_DEC_CARVEOUT 0  // A/B: preferred shared-memory carveout (percent) of k_decode; 0 = driver default
 #endif
@@ -311,6 +314,16 @@ __global__ void __launch_bounds__(256, DecShared<DT>::kMinB) k_decode(const uint
         // ---- a8: warp per block
         for (uint64_t b = seg + warp; b < seg_end; b += kWarps) {
           const unsigned long long off = cbase + run0 + soff[b - seg];
+#if UZIP_DEC_L2PF
+          // A/B: pull the next pair's payload (blocks b + 16 and b + 24; lanes 0-15 / 16-31, 128 B each)
+          // into L2 while this pair decodes
+          if (DS::kPair && b + 3 * kWarps + 1 < seg_end) {
+            const uint64_t nb2 = b + (lane < 16 ? 2 : 3) * kWarps - seg;
+            const unsigned long long o0 = soff[nb2], o1 = soff[nb2 + 1];
+            const unsigned long long at = (unsigned long long)(lane & 15) * 128;
+            if (at < o1 - o0) asm volatile("prefetch.global.L2 [%0];" ::"l"(in + g.off_pay + cbase + run0 + o0 + at));
+          }
+#endif
           if (DS::kPair && b + kWarps < seg_end &&
               decode_pair<DT>(in, g, payload, dir[b], b, off, dir[b + kWarps], b + kWarps,
                               cbase + run0 + soff[b + kWarps - seg], dtab, pay, out, ws)) {
